@@ -1,0 +1,113 @@
+/*
+ * pmh.h -- C ABI of the B200-native ProbMinHash signature engine (libpmh.so).
+ *
+ * Drop-in boundary for the reference's kernel layer
+ *   /root/reference/pkg/src/probminhash/_kernels.py   (K)
+ * which the reference's public API (sketch.py:121-213, estimate.py:91-123)
+ * calls one set at a time as
+ *   K._k_<algo>(ids: uint64[n], weights: float64[n], m) -> (uint64[m], int64[3])
+ * and K._k_sketch_dispatch(algo_id, ids, weights, m) (K:884-917).
+ * Here a call covers a whole CSR batch of sets; a single set is a batch of 1.
+ *
+ * Conventions: plain pointers and sizes only.  Functions named *_host take
+ * host pointers and perform the host<->device copies themselves; all others
+ * take DEVICE pointers, are stream-ordered on `stream` (a cudaStream_t, NULL =
+ * legacy default stream) and synchronise that stream only to report errors.
+ * Algorithm ids are the reference's ALG_* constants (K:866-881).
+ * Return value: PMH_OK or a negative PMH_ERR_* code; *err_set (if non-NULL)
+ * receives the index of the first offending set for EMPTY / RANDOMNESS.
+ */
+#ifndef PMH_H_
+#define PMH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> reference exceptions (errors.py:4-17) */
+#define PMH_OK 0
+#define PMH_ERR_EMPTY (-1)      /* EmptyInputError: a set has no elements   */
+#define PMH_ERR_INVALID (-2)    /* InvalidParamsError: m / algo / b domain  */
+#define PMH_ERR_RANDOMNESS (-3) /* RandomnessFailureError: loop cap hit      */
+#define PMH_ERR_CUDA (-4)       /* CUDA runtime failure (see last_error)    */
+#define PMH_ERR_NOMEM (-5)
+
+/* algorithm ids, K:866-881 */
+#define PMH_ALG_PMINHASH 0
+#define PMH_ALG_PMH1 1
+#define PMH_ALG_PMH1A 2
+#define PMH_ALG_PMH2 3
+#define PMH_ALG_PMH3 4
+#define PMH_ALG_PMH3A 5
+#define PMH_ALG_PMH4 6
+#define PMH_ALG_MINHASH 10
+#define PMH_ALG_SUPERMINHASH 11
+#define PMH_ALG_OPH 12
+#define PMH_ALG_UW1 13
+#define PMH_ALG_UW1A 14
+#define PMH_ALG_UW2 15
+#define PMH_ALG_UW3 16
+#define PMH_ALG_UW3A 17
+#define PMH_ALG_UW4 18
+
+/* library version (major*10000 + minor*100 + patch) */
+int pmh_version(void);
+
+/* human-readable description of the last error on this thread */
+const char* pmh_last_error(void);
+
+/*
+ * Sketch a CSR batch of sets.
+ * Replaces K._k_pminhash (K:284), _k_probminhash1/1a/2/3/3a/4 (K:303-614),
+ * _k_uw_probminhash3/3a/4 (K:619-763) and the unit-weight calls of
+ * sketch_unweighted (sketch.py:188-213), i.e. K._k_sketch_dispatch (K:884).
+ *   ids       uint64[nelems]      element ids, set s = [offsets[s], offsets[s+1])
+ *   weights   float64[nelems]     positive finite weights; ignored (may be NULL)
+ *                                  for the unweighted algorithms (ids 13..18)
+ *   offsets   int64[nsets+1]
+ *   sig_out   uint64[nsets*m]     row-major signatures (element ids)
+ *   stats_out int64[nsets*3] or NULL: [points generated, elements needing more
+ *             than one point (interleaved variants 1a/3a only, else 0),
+ *             successful slot updates] -- GPU-schedule statistics, see DESIGN.md
+ * m >= 1 (m >= 2 for PMH3/3a/4 and UW3/3a/4, sketch.py:148-166,198).
+ */
+int pmh_sketch_csr(int algo, int64_t m, const uint64_t* ids,
+                   const double* weights, const int64_t* offsets,
+                   int64_t nsets, uint64_t* sig_out, int64_t* stats_out,
+                   int64_t* err_set, void* stream);
+
+/* Same with HOST buffers (pageable or pinned); nelems = offsets[nsets]. */
+int pmh_sketch_csr_host(int algo, int64_t m, const uint64_t* ids,
+                        const double* weights, const int64_t* offsets,
+                        int64_t nsets, int64_t nelems, uint64_t* sig_out,
+                        int64_t* stats_out, int64_t* err_set);
+
+/*
+ * Equal-component counts of npairs signature pairs (rows of A and B):
+ * counts[p] = #{k : A[p,k] == B[p,k]}.  estimate_similarity (estimate.py:91-95)
+ * is counts[p] / m.
+ */
+int pmh_count_equal(const uint64_t* a, const uint64_t* b, int64_t npairs,
+                    int64_t m, int32_t* counts, void* stream);
+
+/*
+ * All-pairs tile over n signatures (row-major [n, m]): for rows i in [r0,r1)
+ * and columns j in [c0,c1) with j > i, out[(i-r0)*ld + (j-c0)] = count(i,j).
+ * Entries with j <= i are left untouched.
+ */
+int pmh_allpairs_tile(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0,
+                      int64_t r1, int64_t c0, int64_t c1, uint16_t* out,
+                      int64_t ld, void* stream);
+
+/* b-bit reduction of nsets*m components (estimate.py:105-114, K:851-861). */
+int pmh_bbit(const uint64_t* sig, int64_t nsets, int64_t m, int b,
+             int64_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PMH_H_ */

@@ -1,0 +1,92 @@
+"""Loader and thin typed wrapper of the native library libpmh.so (C ABI in
+include/pmh.h).  The library is built in-tree by __graft_entry__.build()
+(or `python -m paper_1911_00675_b200.build`).  There is no fallback: if the
+library or a CUDA device is missing, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import EmptyInputError, InvalidParamsError, RandomnessFailureError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpmh.so")
+
+PMH_OK = 0
+PMH_ERR_EMPTY = -1
+PMH_ERR_INVALID = -2
+PMH_ERR_RANDOMNESS = -3
+PMH_ERR_CUDA = -4
+PMH_ERR_NOMEM = -5
+
+# reference algorithm ids, K:866-881
+ALG = {
+    "pminhash": 0, "probminhash1": 1, "probminhash1a": 2, "probminhash2": 3,
+    "probminhash3": 4, "probminhash3a": 5, "probminhash4": 6,
+    "minhash": 10, "superminhash": 11, "oph": 12,
+    "unweighted1": 13, "unweighted1a": 14, "unweighted2": 15,
+    "unweighted3": 16, "unweighted3a": 17, "unweighted4": 18,
+}
+UNWEIGHTED_IDS = {10, 11, 12, 13, 14, 15, 16, 17, 18}
+
+# every symbol include/pmh.h declares
+EXPORTS = ("pmh_version", "pmh_last_error", "pmh_sketch_csr", "pmh_sketch_csr_host",
+           "pmh_count_equal", "pmh_allpairs_tile", "pmh_bbit")
+
+_lib = None
+_lock = threading.Lock()
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+class NativeLibraryMissing(RuntimeError):
+    pass
+
+
+def load():
+    """Load libpmh.so (no CUDA context is created)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise NativeLibraryMissing(
+                f"{LIB_PATH} is not built; run __graft_entry__.build() "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        L.pmh_version.restype = ctypes.c_int
+        L.pmh_last_error.restype = ctypes.c_char_p
+        L.pmh_sketch_csr.argtypes = [ctypes.c_int, _i64, _vp, _vp, _vp, _i64, _vp, _vp,
+                                     _i64p, _vp]
+        L.pmh_sketch_csr.restype = ctypes.c_int
+        L.pmh_sketch_csr_host.argtypes = [ctypes.c_int, _i64, _vp, _vp, _vp, _i64, _i64,
+                                          _vp, _vp, _i64p]
+        L.pmh_sketch_csr_host.restype = ctypes.c_int
+        L.pmh_count_equal.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp]
+        L.pmh_count_equal.restype = ctypes.c_int
+        L.pmh_allpairs_tile.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _i64,
+                                        _vp]
+        L.pmh_allpairs_tile.restype = ctypes.c_int
+        L.pmh_bbit.argtypes = [_vp, _i64, _i64, ctypes.c_int, _vp, _vp]
+        L.pmh_bbit.restype = ctypes.c_int
+        _lib = L
+        return L
+
+
+def check(rc: int, err_set: int = -1):
+    """Map a C status to the reference's exception types (errors.py)."""
+    if rc == PMH_OK:
+        return
+    msg = load().pmh_last_error().decode(errors="replace")
+    if rc == PMH_ERR_EMPTY:
+        raise EmptyInputError(msg)
+    if rc == PMH_ERR_INVALID:
+        raise InvalidParamsError(msg)
+    if rc == PMH_ERR_RANDOMNESS:
+        raise RandomnessFailureError(msg)
+    raise RuntimeError(f"libpmh error {rc}: {msg}")

@@ -1,0 +1,161 @@
+"""Batch (CSR) API on the GPU: the engine's native calling convention.
+
+A batch is (ids u64[N], weights f64[N] or None, offsets i64[S+1]).  Inputs may
+be numpy arrays (host; copied to the device) or torch CUDA tensors (device
+resident; int64 tensors carry the u64 ids bit-for-bit).  Signatures come back
+as int64 CUDA tensors (bit-identical to the u64 ids) or numpy uint64 arrays.
+
+Every call goes through libpmh.so (include/pmh.h); there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import EmptyInputError, InvalidParamsError
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1911_00675_b200 needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def algo_id(algo) -> int:
+    if isinstance(algo, str):
+        if algo not in _lib.ALG:
+            raise InvalidParamsError(f"unknown algorithm {algo!r}")
+        return _lib.ALG[algo]
+    return int(algo)
+
+
+def to_device_u64(x, device=None):
+    """numpy uint64 / int64 array or torch tensor -> contiguous int64 CUDA tensor."""
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        t = x if x.dtype == torch.int64 else x.view(torch.int64) if x.dtype == torch.uint64 \
+            else x.to(torch.int64)
+        return t.to(device or "cuda").contiguous()
+    a = np.ascontiguousarray(x)
+    if a.dtype != np.uint64:
+        a = a.astype(np.uint64)
+    return torch.from_numpy(a.view(np.int64)).to(device or "cuda")
+
+
+def to_device_f64(x, device=None):
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        return x.to(device or "cuda", torch.float64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, np.float64)).to(device or "cuda")
+
+
+def to_device_i64(x, device=None):
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        return x.to(device or "cuda", torch.int64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, np.int64)).to(device or "cuda")
+
+
+def _stream_ptr(torch, dev):
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def sketch_csr_device(algo, m: int, ids, weights, offsets, want_stats=True):
+    """Device-resident batch sketch.
+
+    ids: int64 CUDA tensor [N]; weights: float64 CUDA tensor [N] or None;
+    offsets: int64 CUDA tensor [S+1].  Returns (sig int64 [S, m] CUDA tensor,
+    stats int64 [S, 3] CUDA tensor or None)."""
+    torch = _torch()
+    aid = algo_id(algo)
+    nsets = offsets.numel() - 1
+    dev = ids.device
+    sig = torch.empty((max(nsets, 0), m), dtype=torch.int64, device=dev)
+    stats = torch.empty((max(nsets, 0), 3), dtype=torch.int64, device=dev) if want_stats else None
+    if aid in _lib.UNWEIGHTED_IDS:
+        weights = None
+    err = ctypes.c_int64(-1)
+    rc = _lib.load().pmh_sketch_csr(
+        aid, m, ids.data_ptr(), weights.data_ptr() if weights is not None else None,
+        offsets.data_ptr(), nsets, sig.data_ptr(),
+        stats.data_ptr() if stats is not None else None, ctypes.byref(err),
+        _stream_ptr(torch, dev))
+    _lib.check(rc, err.value)
+    return sig, stats
+
+
+def sketch_csr(algo, m: int, ids, weights, offsets, want_stats=True):
+    """Host-array batch sketch -> (sig uint64[S, m], stats int64[S, 3]).
+
+    Goes through the C ABI's host entry point (H2D, kernels, D2H inside)."""
+    aid = algo_id(algo)
+    _torch()  # a CUDA device is required
+    ids = np.ascontiguousarray(ids, np.uint64)
+    offsets = np.ascontiguousarray(offsets, np.int64)
+    nsets = offsets.size - 1
+    if aid in _lib.UNWEIGHTED_IDS or weights is None:
+        w = None
+    else:
+        w = np.ascontiguousarray(weights, np.float64)
+    sig = np.empty((max(nsets, 0), m), np.uint64)
+    stats = np.empty((max(nsets, 0), 3), np.int64) if want_stats else None
+    err = ctypes.c_int64(-1)
+    rc = _lib.load().pmh_sketch_csr_host(
+        aid, m, ids.ctypes.data, w.ctypes.data if w is not None else None,
+        offsets.ctypes.data, nsets, int(offsets[-1]) if nsets > 0 else 0,
+        sig.ctypes.data, stats.ctypes.data if stats is not None else None,
+        ctypes.byref(err))
+    _lib.check(rc, err.value)
+    return sig, stats
+
+
+def count_equal_device(a, b):
+    """a, b: int64 CUDA tensors [P, m] -> int32 CUDA tensor [P] of equal counts."""
+    torch = _torch()
+    if a.shape != b.shape:
+        raise InvalidParamsError("signature sizes differ")
+    P, m = a.shape
+    out = torch.empty(P, dtype=torch.int32, device=a.device)
+    rc = _lib.load().pmh_count_equal(a.contiguous().data_ptr(), b.contiguous().data_ptr(),
+                                     P, m, out.data_ptr(), _stream_ptr(torch, a.device))
+    _lib.check(rc)
+    return out
+
+
+def allpairs_tile_device(sigs, r0, r1, c0, c1, out=None):
+    """Equal-component counts for rows [r0,r1) x cols [c0,c1), upper triangle
+    (j > i); uint16 counts in a (r1-r0, c1-c0) int16 CUDA tensor (zeros
+    elsewhere)."""
+    torch = _torch()
+    n, m = sigs.shape
+    if out is None:
+        out = torch.zeros((r1 - r0, c1 - c0), dtype=torch.int16, device=sigs.device)
+    rc = _lib.load().pmh_allpairs_tile(sigs.contiguous().data_ptr(), n, m, r0, r1, c0, c1,
+                                       out.data_ptr(), out.stride(0),
+                                       _stream_ptr(torch, sigs.device))
+    _lib.check(rc)
+    return out
+
+
+def bbit_device(sig, b: int):
+    torch = _torch()
+    S, m = sig.shape
+    out = torch.empty((S, m), dtype=torch.int64, device=sig.device)
+    rc = _lib.load().pmh_bbit(sig.contiguous().data_ptr(), S, m, b, out.data_ptr(),
+                              _stream_ptr(torch, sig.device))
+    _lib.check(rc)
+    return out
+
+
+def sigs_to_numpy(sig) -> np.ndarray:
+    return sig.cpu().numpy().view(np.uint64)
+
+
+def check_nonempty(offsets):
+    sizes = np.diff(np.asarray(offsets, np.int64))
+    if sizes.size and (sizes <= 0).any():
+        raise EmptyInputError("cannot sketch an empty set")

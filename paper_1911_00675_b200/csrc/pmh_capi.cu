@@ -1,0 +1,337 @@
+// pmh_capi.cu -- extern "C" boundary of libpmh.so (declared in include/pmh.h).
+//
+// Host responsibilities: argument validation with the reference's error
+// domain (sketch.py:96-114), per-(device, m) constant tables computed with the
+// host glibc exactly as the reference computes them inside each call
+// (K:418-420, K:458-459, K:497-498, K:568-579), kernel dispatch, and mapping
+// device error flags to the reference's exceptions (errors.py).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/pmh.h"
+#include "pmh_pminhash.cuh"
+#include "pmh_sketch.cuh"
+
+using namespace pmh;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return set_error(PMH_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define PMH_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+constexpr int ERRF_EMPTY = 4;
+
+// ---- constant tables (glibc on the host, uploaded once per device and m) --
+struct DevTables {
+  Tables t{};
+  void* mem = nullptr;
+};
+
+std::mutex g_mu;
+std::map<std::tuple<int, int, int64_t>, DevTables> g_tables;
+
+void trunc_consts(double lam, TruncExpConsts* c) {  // K:186-191
+  c->lam = lam;
+  c->c1 = std::expm1(lam) / lam;
+  c->c2 = std::log(2.0 / (1.0 + std::exp(-lam))) / lam;
+  c->c3 = -std::expm1(-lam) / lam;
+}
+
+int get_tables(int family, int64_t m, const Tables** out) {
+  int dev = 0;
+  PMH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_tuple(dev, family, m);
+  auto it = g_tables.find(key);
+  if (it != g_tables.end()) { *out = &it->second.t; return PMH_OK; }
+  DevTables dt;
+  if (family == FAM_PMH3 && m >= 2) {
+    trunc_consts(std::log1p(1.0 / ((double)m - 1.0)), &dt.t.c3);  // K:458-459
+  } else if (family == FAM_PMH2) {
+    std::vector<double> beta(m + 1, 0.0);
+    for (int64_t i = 2; i <= m; i++) beta[i] = (double)m / ((double)(m - i) + 1.0);  // K:418-420
+    PMH_CUDA(cudaMalloc(&dt.mem, sizeof(double) * (m + 1)));
+    PMH_CUDA(cudaMemcpy(dt.mem, beta.data(), sizeof(double) * (m + 1), cudaMemcpyHostToDevice));
+    dt.t.beta = (const double*)dt.mem;
+  } else if (family == FAM_PMH4 && m >= 2) {  // K:568-579
+    std::vector<TruncExpConsts> c4(m);
+    std::vector<double> gam(m, 0.0), dgam(m, 0.0);
+    const double lam1 = std::log1p(1.0 / ((double)m - 1.0));
+    for (int64_t i = 1; i < m; i++) {
+      trunc_consts(std::log1p(1.0 / (double)(m - i)), &c4[i]);
+      gam[i] = std::log1p((double)i / (double)(m - i)) / lam1;
+    }
+    for (int64_t i = 1; i < m; i++) dgam[i] = gam[i] - gam[i - 1];
+    c4[0] = c4[m > 1 ? 1 : 0];
+    dt.t.delta = 1.0 / lam1;
+    const size_t bc = sizeof(TruncExpConsts) * m, bg = sizeof(double) * m;
+    PMH_CUDA(cudaMalloc(&dt.mem, bc + 2 * bg));
+    char* p = (char*)dt.mem;
+    PMH_CUDA(cudaMemcpy(p, c4.data(), bc, cudaMemcpyHostToDevice));
+    PMH_CUDA(cudaMemcpy(p + bc, gam.data(), bg, cudaMemcpyHostToDevice));
+    PMH_CUDA(cudaMemcpy(p + bc + bg, dgam.data(), bg, cudaMemcpyHostToDevice));
+    dt.t.c4 = (const TruncExpConsts*)p;
+    dt.t.gam = (const double*)(p + bc);
+    dt.t.dgam = (const double*)(p + bc + bg);
+  }
+  auto res = g_tables.emplace(key, dt);
+  *out = &res.first->second.t;
+  return PMH_OK;
+}
+
+int family_of(int algo) {
+  switch (algo) {
+    case ALG_PMH1: case ALG_PMH1A: case ALG_UW1: case ALG_UW1A: return FAM_PMH1;
+    case ALG_PMH2: case ALG_UW2: return FAM_PMH2;
+    case ALG_PMH3: case ALG_PMH3A: return FAM_PMH3;
+    case ALG_PMH4: return FAM_PMH4;
+    case ALG_UW3: case ALG_UW3A: return FAM_UW3;
+    case ALG_UW4: return FAM_UW4;
+    default: return 0;
+  }
+}
+
+bool is_unweighted(int algo) { return algo >= ALG_UW1; }
+bool reports_buffer(int algo) {
+  return algo == ALG_PMH1A || algo == ALG_PMH3A || algo == ALG_UW1A || algo == ALG_UW3A;
+}
+int64_t min_m(int algo) {
+  switch (algo) {
+    case ALG_PMH3: case ALG_PMH3A: case ALG_PMH4: case ALG_UW3: case ALG_UW3A:
+    case ALG_UW4: case ALG_SUPERMINHASH: return 2;
+    default: return 1;
+  }
+}
+
+template <int F>
+cudaError_t launch_family(const SketchArgs& a, cudaStream_t st) {
+  const int threads = 256;
+  size_t smem = sizeof(Slot) * (size_t)a.m;
+  if (family_uses_fy(F)) smem += (size_t)(threads / 32) * sizeof(int32_t) * (size_t)(a.m + 1);
+  cudaError_t e = cudaFuncSetAttribute(sketch_sets_kernel<F>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = a.nsets < 2147483647LL ? a.nsets : 2147483647LL;
+  sketch_sets_kernel<F><<<(unsigned)grid, threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int C, bool EXPO>
+cudaError_t launch_pmin_c(const PMinArgs& a, cudaStream_t st) {
+  const int tpg = (int)((a.m + C - 1) / C);
+  const int groups = PMIN_THREADS / tpg;
+  const size_t smem = sizeof(Slot) * (size_t)groups * (size_t)a.m;
+  cudaError_t e = cudaFuncSetAttribute(pminhash_kernel<C, EXPO>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = a.nsets < 2147483647LL ? a.nsets : 2147483647LL;
+  pminhash_kernel<C, EXPO><<<(unsigned)grid, PMIN_THREADS, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <bool EXPO>
+cudaError_t launch_pminhash(const PMinArgs& a, cudaStream_t st) {
+  // C = components per thread: smallest power of two with m/C <= 128
+  // (>= 2 groups of threads per CTA), capped at 32 (registers)
+  int64_t c = 1;
+  while (a.m > 128 * c && c < 32) c *= 2;
+  switch (c) {
+    case 1: return launch_pmin_c<1, EXPO>(a, st);
+    case 2: return launch_pmin_c<2, EXPO>(a, st);
+    case 4: return launch_pmin_c<4, EXPO>(a, st);
+    case 8: return launch_pmin_c<8, EXPO>(a, st);
+    case 16: return launch_pmin_c<16, EXPO>(a, st);
+    default: return launch_pmin_c<32, EXPO>(a, st);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int pmh_version(void) { return 100; }
+
+const char* pmh_last_error(void) { return g_last_error.c_str(); }
+
+int pmh_sketch_csr(int algo, int64_t m, const uint64_t* ids,
+                   const double* weights, const int64_t* offsets,
+                   int64_t nsets, uint64_t* sig_out, int64_t* stats_out,
+                   int64_t* err_set, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (err_set) *err_set = -1;
+  const int fam = family_of(algo);
+  if (algo != ALG_PMINHASH && algo != ALG_MINHASH && fam == 0)
+    return set_error(PMH_ERR_INVALID, "unsupported algorithm id " + std::to_string(algo));
+  if (m < min_m(algo))
+    return set_error(PMH_ERR_INVALID, "signature size must be >= " + std::to_string(min_m(algo)));
+  if (m > 65536) return set_error(PMH_ERR_INVALID, "signature size must be <= 65536");
+  if (nsets < 0) return set_error(PMH_ERR_INVALID, "negative set count");
+  if (nsets == 0) return PMH_OK;
+  if (!is_unweighted(algo) && !weights)
+    return set_error(PMH_ERR_INVALID, "weighted algorithm requires weights");
+
+  int* d_flags = nullptr;
+  PMH_CUDA(cudaMallocAsync((void**)&d_flags, 16, st));
+  long long* d_err_set = (long long*)((char*)d_flags + 8);
+  const long long init_set = 0x7FFFFFFFFFFFFFFFLL;
+  PMH_CUDA(cudaMemsetAsync(d_flags, 0, 8, st));
+  PMH_CUDA(cudaMemcpyAsync(d_err_set, &init_set, 8, cudaMemcpyHostToDevice, st));
+
+  cudaError_t e;
+  if (algo == ALG_PMINHASH || algo == ALG_MINHASH) {
+    PMinArgs a{ids, algo == ALG_PMINHASH ? weights : nullptr, offsets, nullptr, nsets, m,
+               sig_out, stats_out, d_err_set};
+    e = algo == ALG_PMINHASH ? launch_pminhash<true>(a, st) : launch_pminhash<false>(a, st);
+  } else {
+    const Tables* tp = nullptr;
+    int rc = get_tables(fam, m, &tp);
+    if (rc) { cudaFreeAsync(d_flags, st); return rc; }
+    SketchArgs a{};
+    a.ids = ids;
+    a.w = is_unweighted(algo) ? nullptr : weights;
+    a.offsets = offsets;
+    a.order = nullptr;
+    a.nsets = nsets;
+    a.m = m;
+    a.sig = sig_out;
+    a.stats = stats_out;
+    a.err_flags = d_flags;
+    a.err_set = d_err_set;
+    a.T = *tp;
+    a.tconst = 4.0;
+    switch (fam) {
+      case FAM_PMH1: e = launch_family<FAM_PMH1>(a, st); break;
+      case FAM_PMH2: e = launch_family<FAM_PMH2>(a, st); break;
+      case FAM_PMH3: e = launch_family<FAM_PMH3>(a, st); break;
+      case FAM_PMH4: e = launch_family<FAM_PMH4>(a, st); break;
+      case FAM_UW3: e = launch_family<FAM_UW3>(a, st); break;
+      default: e = launch_family<FAM_UW4>(a, st); break;
+    }
+  }
+  if (e != cudaSuccess) { cudaFreeAsync(d_flags, st); return cuda_fail(e, "kernel launch"); }
+  if (stats_out && !reports_buffer(algo) && algo != ALG_PMINHASH && algo != ALG_MINHASH) {
+    // the non-interleaved variants have no buffer (K:334-336): column 1 = 0
+    PMH_CUDA(cudaMemset2DAsync(stats_out + 1, 3 * sizeof(int64_t), 0, sizeof(int64_t),
+                               (size_t)nsets, st));
+  }
+  int h_flags[4] = {0, 0, 0, 0};
+  PMH_CUDA(cudaMemcpyAsync(h_flags, d_flags, 16, cudaMemcpyDeviceToHost, st));
+  PMH_CUDA(cudaFreeAsync(d_flags, st));
+  PMH_CUDA(cudaStreamSynchronize(st));
+  long long bad;
+  memcpy(&bad, &h_flags[2], 8);
+  if (bad != init_set) {
+    if (err_set) *err_set = bad;
+    if (h_flags[0] & ERRF_RANDOMNESS)
+      return set_error(PMH_ERR_RANDOMNESS, "rejection or coupon loop exceeded its cap in set " +
+                                               std::to_string(bad));
+    return set_error(PMH_ERR_EMPTY, "cannot sketch an empty set (set " + std::to_string(bad) + ")");
+  }
+  return PMH_OK;
+}
+
+int pmh_sketch_csr_host(int algo, int64_t m, const uint64_t* ids,
+                        const double* weights, const int64_t* offsets,
+                        int64_t nsets, int64_t nelems, uint64_t* sig_out,
+                        int64_t* stats_out, int64_t* err_set) {
+  if (nsets <= 0 || nelems < 0) {
+    if (nsets == 0) return PMH_OK;
+    return set_error(PMH_ERR_INVALID, "negative sizes");
+  }
+  cudaStream_t st;
+  PMH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const bool weighted = !is_unweighted(algo) && weights;
+  const size_t bi = sizeof(uint64_t) * (size_t)nelems, bw = weighted ? sizeof(double) * (size_t)nelems : 0,
+               bo = sizeof(int64_t) * (size_t)(nsets + 1), bs = sizeof(uint64_t) * (size_t)nsets * (size_t)m,
+               bst = stats_out ? sizeof(int64_t) * 3 * (size_t)nsets : 0;
+  char* d = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&d, bi + bw + bo + bs + bst + 64, st);
+  if (e != cudaSuccess) { cudaStreamDestroy(st); return cuda_fail(e, "cudaMallocAsync"); }
+  uint64_t* d_ids = (uint64_t*)d;
+  double* d_w = (double*)(d + bi);
+  int64_t* d_off = (int64_t*)(d + bi + bw);
+  uint64_t* d_sig = (uint64_t*)(d + bi + bw + bo);
+  int64_t* d_stats = stats_out ? (int64_t*)(d + bi + bw + bo + bs) : nullptr;
+  int rc = PMH_OK;
+  if ((e = cudaMemcpyAsync(d_ids, ids, bi, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+      (weighted && (e = cudaMemcpyAsync(d_w, weights, bw, cudaMemcpyHostToDevice, st)) != cudaSuccess) ||
+      (e = cudaMemcpyAsync(d_off, offsets, bo, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+    rc = cuda_fail(e, "H2D");
+  }
+  if (rc == PMH_OK)
+    rc = pmh_sketch_csr(algo, m, d_ids, weighted ? d_w : nullptr, d_off, nsets, d_sig, d_stats,
+                        err_set, st);
+  if (rc == PMH_OK) {
+    if ((e = cudaMemcpyAsync(sig_out, d_sig, bs, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (stats_out && (e = cudaMemcpyAsync(stats_out, d_stats, bst, cudaMemcpyDeviceToHost, st)) != cudaSuccess))
+      rc = cuda_fail(e, "D2H");
+  }
+  cudaFreeAsync(d, st);
+  e = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (rc == PMH_OK && e != cudaSuccess) rc = cuda_fail(e, "sync");
+  return rc;
+}
+
+int pmh_count_equal(const uint64_t* a, const uint64_t* b, int64_t npairs,
+                    int64_t m, int32_t* counts, void* stream) {
+  if (m < 1 || npairs < 0) return set_error(PMH_ERR_INVALID, "bad sizes");
+  if (npairs == 0) return PMH_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int threads = 256;
+  int64_t blocks = (npairs * 32 + threads - 1) / threads;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  count_equal_kernel<<<(unsigned)blocks, threads, 0, st>>>(a, b, npairs, m, counts);
+  PMH_CUDA(cudaGetLastError());
+  return PMH_OK;
+}
+
+int pmh_allpairs_tile(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0,
+                      int64_t r1, int64_t c0, int64_t c1, uint16_t* out,
+                      int64_t ld, void* stream) {
+  if (m < 1 || m > 65535 || r0 < 0 || r1 > n || c0 < 0 || c1 > n || r0 > r1 || c0 > c1)
+    return set_error(PMH_ERR_INVALID, "bad tile bounds");
+  if (r0 == r1 || c0 == c1) return PMH_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 grid((unsigned)((c1 - c0 + AP_TILE - 1) / AP_TILE), (unsigned)((r1 - r0 + AP_TILE - 1) / AP_TILE));
+  allpairs_tile_kernel<<<grid, 256, 0, st>>>(sigs, n, m, r0, r1, c0, c1, out, ld);
+  PMH_CUDA(cudaGetLastError());
+  return PMH_OK;
+}
+
+int pmh_bbit(const uint64_t* sig, int64_t nsets, int64_t m, int b, int64_t* out,
+             void* stream) {
+  if (b < 1 || b > 16) return set_error(PMH_ERR_INVALID, "b must be in 1..16");
+  if (m < 1 || nsets < 0) return set_error(PMH_ERR_INVALID, "bad sizes");
+  const int64_t total = nsets * m;
+  if (total == 0) return PMH_OK;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  bbit_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(sig, total, m, b, out);
+  PMH_CUDA(cudaGetLastError());
+  return PMH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,517 @@
+// pmh_sketch.cuh -- ProbMinHash signature kernels (sm_100a).
+//
+// One CTA per set (grid-stride over a cost-ordered set list).  Shared memory
+// holds the set's slot table (lexicographic argmin of (h, element index) per
+// component, 128-bit CAS) and the stop limit h_max.  Because a signature is
+//   sig_k = argmin_d (h_k(d), index(d))
+// over per-element point sequences that are fixed functions of (id, w, m,
+// variant), and early stopping only skips points above the final stop limit
+// H, elements may be processed in ANY order with ANY threshold >= H
+// (SURVEY.md §0 facts 4 and 6).  Each CTA therefore:
+//   1. computes W = sum(w) and a threshold guess t = m (ln m + 4) / W
+//      (a point-process estimate of H; correctness never depends on it);
+//   2. streams elements, one per thread, through the variant's exact point
+//      recurrence (Appendix A), skipping every point whose value -- or a
+//      provable lower bound of it, which avoids log1p -- exceeds
+//      thr = min(t, h_max);
+//   3. hands elements whose lazy Fisher-Yates state outgrows the per-thread
+//      sparse map to warp-cooperative processing with a dense shared map;
+//   4. verifies max_k h_k <= t (else retries with a larger t; re-offering a
+//      point is idempotent) and writes sig_k = ids[argmin].
+#pragma once
+#include <stdint.h>
+
+#include "pmh_device.cuh"
+
+namespace pmh {
+
+// per-m constant tables computed on the host with glibc (K:186-191,
+// K:418-420, K:458-459, K:568-579)
+struct Tables {
+  TruncExpConsts c3;          // PMH3: lam = log1p(1/(m-1))
+  const TruncExpConsts* c4;   // PMH4: [m] per interval, index 1..m-1
+  const double* gam;          // PMH4: gamma_i, [m]
+  const double* dgam;         // PMH4: fl(gamma_i - gamma_{i-1}), [m]
+  double delta;               // PMH4: 1/lam_1
+  const double* beta;         // PMH2: [m+1], beta_i = m/(m-i+1.0)
+};
+
+struct SetCtx {
+  Slot* slots;                       // [m] shared
+  unsigned long long* hmax_bits;     // shared, current upper bound of H
+  unsigned int* filled;              // shared, #non-empty slots
+  double tguess;                     // current threshold guess
+  int64_t m;
+  uint32_t kbits;
+  int64_t cap;                       // coupon cap K:279-281
+  // counters (per thread)
+  int64_t points;
+  int64_t updates;
+  int64_t multi;                     // elements that produced > 1 point
+};
+
+__device__ __forceinline__ double ctx_thr(const SetCtx& c) {
+  const double h = __longlong_as_double((long long)*(volatile unsigned long long*)c.hmax_bits);
+  return h < c.tguess ? h : c.tguess;
+}
+
+// serial exact recompute of max_k h_k (rare: triggered when the last empty
+// slot fills or when the slot holding the maximum is lowered)
+__device__ __noinline__ void hmax_recompute_serial(SetCtx& c) {
+  unsigned long long mx = 0;
+  for (int64_t k = 0; k < c.m; k++) {
+    unsigned long long h = *(volatile unsigned long long*)&c.slots[k].h;
+    mx = h > mx ? h : mx;
+  }
+  atomicMin(c.hmax_bits, mx);
+}
+
+__device__ __forceinline__ void ctx_offer(SetCtx& c, int64_t k0, double x,
+                                          int64_t e) {
+  unsigned long long prev = slot_offer(&c.slots[k0], x, (unsigned long long)e);
+  if (prev == ~0ULL) return;
+  c.updates++;
+  if (prev == EMPTY_H) {
+    unsigned f = atomicAdd(c.filled, 1u) + 1u;
+    if (f == (unsigned)c.m) hmax_recompute_serial(c);
+  } else if (prev >= *(volatile unsigned long long*)c.hmax_bits) {
+    hmax_recompute_serial(c);
+  }
+}
+
+// warp-cooperative refresh of h_max
+__device__ __forceinline__ void hmax_refresh_warp(SetCtx& c, int lane) {
+  if (*(volatile unsigned*)c.filled < (unsigned)c.m) return;
+  unsigned long long mx = 0;
+  for (int64_t k = lane; k < c.m; k += 32) {
+    unsigned long long h = *(volatile unsigned long long*)&c.slots[k].h;
+    mx = h > mx ? h : mx;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = v > mx ? v : mx;
+  }
+  if (lane == 0) atomicMin(c.hmax_bits, mx);
+}
+
+// ---------------------------------------------------------------------------
+// Lazy Fisher-Yates (K:222-235).  Positions/values are 1-based; an absent
+// entry means perm[p] == p.
+// ---------------------------------------------------------------------------
+constexpr int SPARSE_FY_CAP = 8;
+
+struct SparseFY {
+  int32_t pos[SPARSE_FY_CAP];
+  int32_t val[SPARSE_FY_CAP];
+  int cnt;
+  __device__ __forceinline__ void reset() { cnt = 0; }
+  __device__ __forceinline__ int32_t get(int32_t p) const {
+    for (int q = 0; q < cnt; q++) if (pos[q] == p) return val[q];
+    return p;
+  }
+  // returns false on overflow
+  __device__ __forceinline__ bool set(int32_t p, int32_t v) {
+    for (int q = 0; q < cnt; q++) if (pos[q] == p) { val[q] = v; return true; }
+    if (cnt == SPARSE_FY_CAP) return false;
+    pos[cnt] = p; val[cnt] = v; cnt++;
+    return true;
+  }
+};
+
+struct DenseFY {  // shared memory, 0 == untouched
+  int32_t* a;
+  __device__ __forceinline__ int32_t get(int32_t p) const {
+    int32_t v = a[p];
+    return v ? v : p;
+  }
+  __device__ __forceinline__ bool set(int32_t p, int32_t v) { a[p] = v; return true; }
+};
+
+// Returns label k (1-based), 0 on FY overflow, -1 on randomness failure.
+template <class FY>
+__device__ __forceinline__ int64_t perm_next(Stream& st, FY& fy, int64_t i,
+                                             int64_t m) {
+  int64_t r = uniform_int(st, m - i + 1);
+  if (r < 0) return -1;
+  int32_t j = (int32_t)(i + r);
+  int32_t k = fy.get(j);
+  if (!fy.set(j, fy.get((int32_t)i))) return 0;
+  return k;
+}
+
+// result codes of the element processors
+constexpr int EL_DONE = 0;
+constexpr int EL_NEED_WARP = 1;
+constexpr int EL_FAIL = -1;
+
+// ---------------------------------------------------------------------------
+// Element processors: the reference recurrences (Appendix A) with the stop
+// test `x >= nodes[root]` replaced by `x > thr` (thr >= H; ties processed).
+// ---------------------------------------------------------------------------
+
+// ProbMinHash1 / 1a / unweighted 1, 1a (K:315-333, K:357-400)
+__device__ __forceinline__ int el_pmh1(SetCtx& c, int64_t e, uint64_t id,
+                                       double winv) {
+  Stream st; st.seed(id);
+  uint64_t b = st.next53();
+  c.points++;
+  if (exp1_scaled_lower_bound(winv, b) > ctx_thr(c)) return EL_DONE;
+  double x = winv * exp1_from_bits(b);
+  int64_t cnt = 1;
+  while (x <= ctx_thr(c)) {
+    int64_t r = uniform_int_masked(st, (uint64_t)c.m, c.kbits);
+    if (r < 0) return EL_FAIL;
+    ctx_offer(c, r, x, e);
+    b = st.next53();
+    c.points++;
+    if (cnt == 1) c.multi++;
+    if (++cnt > c.cap) return EL_FAIL;
+    if (x + exp1_scaled_lower_bound(winv, b) > ctx_thr(c)) return EL_DONE;
+    x = x + winv * exp1_from_bits(b);
+  }
+  return EL_DONE;
+}
+
+// ProbMinHash2 / unweighted 2 (K:423-441)
+template <class FY>
+__device__ __forceinline__ int el_pmh2(SetCtx& c, const Tables& T, FY& fy,
+                                       int64_t e, uint64_t id, double winv) {
+  Stream st; st.seed(id);
+  uint64_t b = st.next53();
+  c.points++;
+  if (exp1_scaled_lower_bound(winv, b) > ctx_thr(c)) return EL_DONE;
+  double x = winv * exp1_from_bits(b);
+  int64_t i = 1;
+  while (x <= ctx_thr(c)) {
+    int64_t k = perm_next(st, fy, i, c.m);
+    if (k <= 0) return k == 0 ? EL_NEED_WARP : EL_FAIL;
+    ctx_offer(c, k - 1, x, e);
+    i++;
+    if (i > c.m) break;
+    const double a = winv * __ldg(&T.beta[i]);
+    b = st.next53();
+    c.points++;
+    if (i == 2) c.multi++;
+    if (x + exp1_scaled_lower_bound(a, b) > ctx_thr(c)) return EL_DONE;
+    x = x + a * exp1_from_bits(b);
+  }
+  return EL_DONE;
+}
+
+// ProbMinHash3 / 3a (K:462-481, K:506-547)
+__device__ __forceinline__ int el_pmh3(SetCtx& c, const Tables& T, int64_t e,
+                                       uint64_t id, double winv) {
+  Stream st; st.seed(id);
+  bool fail = false;
+  double x = winv * trunc_exp(st, T.c3, &fail);
+  c.points++;
+  int64_t i = 1;
+  while (x <= ctx_thr(c)) {
+    int64_t r = uniform_int_masked(st, (uint64_t)c.m, c.kbits);
+    if (r < 0 || fail) return EL_FAIL;
+    ctx_offer(c, r, x, e);
+    if (++i > c.cap) return EL_FAIL;
+    x = winv * ((double)i - 1.0);
+    if (x > ctx_thr(c)) break;
+    x = x + winv * trunc_exp(st, T.c3, &fail);
+    c.points++;
+    if (i == 2) c.multi++;
+  }
+  return fail ? EL_FAIL : EL_DONE;
+}
+
+// ProbMinHash4 (K:582-610)
+template <class FY>
+__device__ __forceinline__ int el_pmh4(SetCtx& c, const Tables& T, FY& fy,
+                                       int64_t e, uint64_t id, double winv) {
+  Stream st; st.seed(id);
+  bool fail = false;
+  double x = winv * trunc_exp(st, T.c4[1], &fail);
+  c.points++;
+  int64_t i = 1;
+  const int64_t m = c.m;
+  while (x <= ctx_thr(c)) {
+    if (fail) return EL_FAIL;
+    int64_t k = perm_next(st, fy, i, m);
+    if (k <= 0) return k == 0 ? EL_NEED_WARP : EL_FAIL;
+    ctx_offer(c, k - 1, x, e);
+    i++;
+    if (winv * __ldg(&T.gam[i - 1]) > ctx_thr(c)) break;
+    if (i == 2) c.multi++;
+    if (i < m) {
+      const double t = trunc_exp(st, T.c4[i], &fail);
+      x = winv * (__ldg(&T.gam[i - 1]) + __ldg(&T.dgam[i]) * t);
+      c.points++;
+    } else {
+      x = winv * (__ldg(&T.gam[m - 1]) + T.delta * exp1_from_bits(st.next53()));
+      c.points++;
+      if (x <= ctx_thr(c)) {
+        k = perm_next(st, fy, m, m);
+        if (k <= 0) return k == 0 ? EL_NEED_WARP : EL_FAIL;
+        ctx_offer(c, k - 1, x, e);
+      }
+      break;
+    }
+  }
+  return fail ? EL_FAIL : EL_DONE;
+}
+
+// unweighted ProbMinHash3 / 3a (K:631-649, K:674-710)
+__device__ __forceinline__ int el_uw3(SetCtx& c, int64_t e, uint64_t id) {
+  Stream st; st.seed(id);
+  double x = st.uniform01();
+  c.points++;
+  int64_t i = 1;
+  while (x <= ctx_thr(c)) {
+    int64_t r = uniform_int_masked(st, (uint64_t)c.m, c.kbits);
+    if (r < 0) return EL_FAIL;
+    ctx_offer(c, r, x, e);
+    if (++i > c.cap) return EL_FAIL;
+    x = (double)i - 1.0;
+    if (x > ctx_thr(c)) break;
+    x = x + st.uniform01();
+    c.points++;
+    if (i == 2) c.multi++;
+  }
+  return EL_DONE;
+}
+
+// unweighted ProbMinHash4 (K:734-759)
+template <class FY>
+__device__ __forceinline__ int el_uw4(SetCtx& c, FY& fy, int64_t e, uint64_t id) {
+  Stream st; st.seed(id);
+  double x = st.uniform01();
+  c.points++;
+  int64_t i = 1;
+  const int64_t m = c.m;
+  while (x <= ctx_thr(c)) {
+    int64_t k = perm_next(st, fy, i, m);
+    if (k <= 0) return k == 0 ? EL_NEED_WARP : EL_FAIL;
+    ctx_offer(c, k - 1, x, e);
+    i++;
+    if ((double)i - 1.0 > ctx_thr(c)) break;
+    if (i == 2) c.multi++;
+    if (i < m) {
+      x = ((double)i - 1.0) + st.uniform01();
+      c.points++;
+    } else {
+      x = ((double)m - 1.0) + st.uniform01();
+      c.points++;
+      if (x <= ctx_thr(c)) {
+        k = perm_next(st, fy, m, m);
+        if (k <= 0) return k == 0 ? EL_NEED_WARP : EL_FAIL;
+        ctx_offer(c, k - 1, x, e);
+      }
+      break;
+    }
+  }
+  return EL_DONE;
+}
+
+// kernel-family selector
+enum Family : int { FAM_PMH1 = 1, FAM_PMH2 = 2, FAM_PMH3 = 3, FAM_PMH4 = 4,
+                    FAM_UW3 = 5, FAM_UW4 = 6 };
+
+__host__ __device__ constexpr bool family_uses_fy(int f) {
+  return f == FAM_PMH2 || f == FAM_PMH4 || f == FAM_UW4;
+}
+__host__ __device__ constexpr bool family_weighted(int f) {
+  return f == FAM_PMH1 || f == FAM_PMH2 || f == FAM_PMH3 || f == FAM_PMH4;
+}
+
+template <int F, class FY>
+__device__ __forceinline__ int run_element(SetCtx& c, const Tables& T, FY& fy,
+                                           int64_t e, uint64_t id, double winv) {
+  if constexpr (F == FAM_PMH1) return el_pmh1(c, e, id, winv);
+  else if constexpr (F == FAM_PMH2) return el_pmh2(c, T, fy, e, id, winv);
+  else if constexpr (F == FAM_PMH3) return el_pmh3(c, T, e, id, winv);
+  else if constexpr (F == FAM_PMH4) return el_pmh4(c, T, fy, e, id, winv);
+  else if constexpr (F == FAM_UW3) return el_uw3(c, e, id);
+  else return el_uw4(c, fy, e, id);
+}
+
+struct SketchArgs {
+  const uint64_t* ids;
+  const double* w;          // nullptr => unit weights
+  const int64_t* offsets;
+  const int32_t* order;     // set processing order (nullptr => identity)
+  int64_t nsets;
+  int64_t m;
+  uint64_t* sig;            // [nsets, m]
+  int64_t* stats;           // [nsets, 3] or nullptr
+  int* err_flags;           // device, OR of ERRF_*
+  long long* err_set;       // device, min failing set index
+  Tables T;
+  double tconst;            // threshold-guess constant (ln m + tconst)
+};
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+__device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? red[lane] : 0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+// Dynamic shared memory layout: Slot[m] | int32 FY[nwarps][m+1] (FY families)
+template <int F>
+__global__ void __launch_bounds__(256) sketch_sets_kernel(SketchArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned long long s_hmax;
+  __shared__ unsigned int s_filled;
+  __shared__ unsigned int s_next;
+  __shared__ int s_retry;
+  __shared__ double s_red[32];
+  __shared__ long long s_redl[32];
+
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int64_t m = a.m;
+  Slot* slots = reinterpret_cast<Slot*>(smem);
+  int32_t* fy_dense = reinterpret_cast<int32_t*>(smem + sizeof(Slot) * m) +
+                      (size_t)wid * (m + 1);
+
+  for (int64_t bs = blockIdx.x; bs < a.nsets; bs += gridDim.x) {
+    const int64_t s = a.order ? (int64_t)a.order[bs] : bs;
+    const int64_t off = a.offsets[s];
+    const int64_t n = a.offsets[s + 1] - off;
+    if (n <= 0) {
+      if (threadIdx.x == 0) atomicMin(a.err_set, (long long)s);
+      continue;
+    }
+    const uint64_t* ids = a.ids + off;
+    const double* w = a.w ? a.w + off : nullptr;
+
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+      slots[k].h = EMPTY_H;
+      slots[k].idx = EMPTY_IDX;
+    }
+    // W = sum of weights (unit weights: n)
+    double W;
+    if (family_weighted(F) && w) {
+      double part = 0.0;
+      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) part += w[e];
+      W = block_sum(part, s_red);
+    } else {
+      W = (double)n;
+    }
+    if (threadIdx.x == 0) { s_hmax = EMPTY_H; s_filled = 0; }
+
+    SetCtx c;
+    c.slots = slots;
+    c.hmax_bits = &s_hmax;
+    c.filled = &s_filled;
+    c.m = m;
+    c.kbits = bits_for(m);
+    c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
+    c.points = 0; c.updates = 0; c.multi = 0;
+    double tg = (double)m * (log((double)m) + a.tconst) / W;
+    if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
+    bool failed = false;
+
+    for (int attempt = 0;; attempt++) {
+      c.tguess = tg;
+      if (threadIdx.x == 0) s_next = 0;
+      __syncthreads();
+      for (;;) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(&s_next, 32u);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if ((int64_t)base >= n) break;
+        const int64_t e = (int64_t)base + lane;
+        int status = EL_DONE;
+        if (e < n) {
+          const uint64_t id = ids[e];
+          const double winv = (family_weighted(F) && w) ? 1.0 / w[e] : 1.0;
+          SparseFY fy; fy.reset();
+          status = run_element<F>(c, a.T, fy, e, id, winv);
+        }
+        if (status == EL_FAIL) failed = true;
+        if constexpr (family_uses_fy(F)) {
+          unsigned heavy = __ballot_sync(0xffffffffu, status == EL_NEED_WARP);
+          while (heavy) {
+            const int l = __ffs(heavy) - 1;
+            heavy &= heavy - 1;
+            const int64_t eh = __shfl_sync(0xffffffffu, e, l);
+            for (int64_t p = lane; p <= m; p += 32) fy_dense[p] = 0;
+            __syncwarp();
+            if (lane == 0) {
+              DenseFY fy{fy_dense};
+              const double winv = (family_weighted(F) && w) ? 1.0 / w[eh] : 1.0;
+              int st = run_element<F>(c, a.T, fy, eh, ids[eh], winv);
+              if (st != EL_DONE) failed = true;
+            }
+            __syncwarp();
+          }
+        }
+        hmax_refresh_warp(c, lane);
+      }
+      __syncthreads();
+      // verification: every slot non-empty and <= tguess
+      unsigned long long mx = 0;
+      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+        unsigned long long h = slots[k].h;
+        mx = h > mx ? h : mx;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = v > mx ? v : mx;
+      }
+      if (threadIdx.x == 0) s_retry = 0;
+      __syncthreads();
+      if (lane == 0 && __longlong_as_double((long long)mx) > tg) atomicOr(&s_retry, 1);
+      const int any_fail = __syncthreads_or(failed ? 1 : 0);
+      if (any_fail) { failed = true; break; }
+      if (!s_retry) break;
+      tg = attempt >= 2 ? __longlong_as_double(0x7FF0000000000000LL) : tg * 4.0;
+      __syncthreads();
+    }
+    if (failed) {
+      if (threadIdx.x == 0) {
+        atomicOr(a.err_flags, ERRF_RANDOMNESS);
+        atomicMin(a.err_set, (long long)s);
+      }
+    }
+    // output
+    uint64_t* sig = a.sig + (size_t)s * m;
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+      const unsigned long long ix = slots[k].idx;
+      sig[k] = ix < (unsigned long long)n ? ids[ix] : 0ULL;
+    }
+    if (a.stats) {
+      long long pts = block_sum_ll(c.points, s_redl);
+      long long mul = block_sum_ll(c.multi, s_redl);
+      long long upd = block_sum_ll(c.updates, s_redl);
+      if (threadIdx.x == 0) {
+        a.stats[s * 3 + 0] = pts;
+        a.stats[s * 3 + 1] = mul;
+        a.stats[s * 3 + 2] = upd;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace pmh

@@ -1,0 +1,72 @@
+"""GPU parity: libpmh.so signatures vs the reference's golden vectors and vs
+the CPU oracle, bit-exact (integer ids).  Calls go through the C ABI."""
+import numpy as np
+import pytest
+
+from golden_io import config_cases, unweighted_cases, weighted_cases
+
+pytestmark = pytest.mark.gpu
+
+GPU_ALGOS = {"pminhash", "probminhash1", "probminhash1a", "probminhash2", "probminhash3",
+             "probminhash3a", "probminhash4", "unweighted1", "unweighted1a", "unweighted2",
+             "unweighted3", "unweighted3a", "unweighted4", "minhash"}
+
+
+def _gpu_sig(algo, m, batch):
+    from paper_1911_00675_b200 import sketch_batch
+    from paper_1911_00675_b200.batch import (sigs_to_numpy, to_device_f64, to_device_i64,
+                                             to_device_u64)
+    ids = to_device_u64(batch.ids)
+    w = to_device_f64(batch.weights) if batch.weights is not None else None
+    off = to_device_i64(batch.offsets)
+    sig, stats = sketch_batch(algo, ids, w, off, m)
+    return sigs_to_numpy(sig), stats.cpu().numpy()
+
+
+def _check(algo, m, batch, sig):
+    if algo not in GPU_ALGOS:
+        pytest.skip(f"{algo} not on the GPU path")
+    got, _ = _gpu_sig(algo, m, batch)
+    ok = np.ones(sig.shape[0], bool)
+    if sig.shape[0] == batch.nsets:
+        pass
+    mism = (got[: sig.shape[0]] != sig)
+    # rows the reference did not run (stats -1) are all-zero in the fixture
+    ran = sig.any(axis=1) | (sig.shape[1] == 0)
+    mism = mism[ran]
+    assert mism.sum() == 0, f"{int(mism.sum())} of {mism.size} components differ"
+
+
+@pytest.mark.parametrize("case", list(weighted_cases()), ids=lambda c: f"{c[0]}-m{c[1]}-{c[3]}")
+def test_weighted_vs_golden(case):
+    key, m, batch, algo, sig, stats = case
+    _check(algo, m, batch, sig)
+
+
+@pytest.mark.parametrize("case", list(unweighted_cases()), ids=lambda c: f"{c[0]}-m{c[1]}-{c[3]}")
+def test_unweighted_vs_golden(case):
+    key, m, batch, algo, sig, stats = case
+    _check(algo, m, batch, sig)
+
+
+@pytest.mark.parametrize("case", list(config_cases()), ids=lambda c: f"{c[0]}-{c[3]}")
+def test_configs_vs_golden(case):
+    key, m, batch, algo, sig, stats = case
+    _check(algo, m, batch, sig)
+
+
+@pytest.mark.parametrize("algo", ["pminhash", "probminhash1", "probminhash2", "probminhash3",
+                                  "probminhash4"])
+@pytest.mark.parametrize("dist", ["uniform", "pareto1.5", "wide"])
+def test_random_vs_oracle(algo, dist):
+    from oracle import oracle as orc
+    from paper_1911_00675_b200 import datagen
+    rng = np.random.default_rng(hash((algo, dist)) & 0xFFFF)
+    sizes = np.exp(rng.uniform(0, np.log(20000), 40)).astype(np.int64) + 1
+    if algo == "pminhash":
+        sizes = np.minimum(sizes, 2000)
+    batch = datagen.random_sets(int(rng.integers(1 << 30)), sizes, dist)
+    for m in (64, 1024):
+        ref, _ = orc.sketch_csr(algo, m, batch.ids, batch.weights, batch.offsets, threads=8)
+        got, _ = _gpu_sig(algo, m, batch)
+        assert (got != ref).sum() == 0
