@@ -113,7 +113,7 @@ int family_of(int algo) {
   }
 }
 
-bool is_unweighted(int algo) { return algo >= ALG_UW1; }
+bool is_unweighted(int algo) { return algo >= ALG_MINHASH; }
 bool reports_buffer(int algo) {
   return algo == ALG_PMH1A || algo == ALG_PMH3A || algo == ALG_UW1A || algo == ALG_UW3A;
 }

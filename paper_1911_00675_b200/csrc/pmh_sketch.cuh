@@ -81,7 +81,9 @@ __device__ __forceinline__ void ctx_offer(SetCtx& c, int64_t k0, double x,
 
 // warp-cooperative refresh of h_max
 __device__ __forceinline__ void hmax_refresh_warp(SetCtx& c, int lane) {
-  if (*(volatile unsigned*)c.filled < (unsigned)c.m) return;
+  // warp-uniform decision (lanes may arrive unconverged after divergent work)
+  const unsigned f = __shfl_sync(0xffffffffu, *(volatile unsigned*)c.filled, 0);
+  if (f < (unsigned)c.m) return;
   unsigned long long mx = 0;
   for (int64_t k = lane; k < c.m; k += 32) {
     unsigned long long h = *(volatile unsigned long long*)&c.slots[k].h;
