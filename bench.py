@@ -1,0 +1,342 @@
+"""Benchmark: set elements hashed/sec at m=1024 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the headline): 10,000 weighted sets with
+log-uniform sizes in [1, 100000] (~8.7e7 elements), uniform (0,1] weights,
+seeded synthetic data (datagen.config2).  One STEP = the whole batch sketched
+once by each of the 7 weighted variants (P-MinHash, ProbMinHash 1, 1a, 2, 3,
+3a, 4) at m = 1024; value = 7 * elements / step time (whole job; N>1 ranks
+each own a full batch -> weak scaling, no collective on this path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Timing: CUDA events on the launching stream, barrier + synchronize on both
+sides, max over ranks.  Inputs (1.47 GB) exceed the 126 MB L2 between steps.
+`e2e` re-measures the metric through the C ABI host entry point
+(pmh_sketch_csr_host) with pinned host inputs: H2D of ids/weights/offsets and
+D2H of the signatures inside the timed region, per variant call.
+`--impl reference` times the reference algorithm's CPU implementation (the C
+restatement in oracle/, pinned bit-exact to the numba reference) on the host
+cores, over a bounded stratified sample of the same batch.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M = 1024
+VARIANTS = ["pminhash", "probminhash1", "probminhash1a", "probminhash2",
+            "probminhash3", "probminhash3a", "probminhash4"]
+METRIC = "set elements hashed/sec at m=1024"
+UNIT = "elements/s"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            bits = [pynvml.nvmlClocksThrottleReasonHwSlowdown,
+                    pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksThrottleReasonSwThermalSlowdown,
+                    pynvml.nvmlClocksThrottleReasonSwPowerCap]
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append([str(sm), str(mx)] +
+                                    ["Active" if r & b else "Not Active" for b in bits])
+                self._stop.wait(0.1)
+            return
+        except Exception:
+            pass
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def algorithmic_bytes(nelems, nsets, m, weighted=True):
+    # 16 B/elt (8 if ids only) + 8 m B/set + 8 (S+1) offsets
+    return (16 if weighted else 8) * nelems + 8 * m * nsets + 8 * (nsets + 1)
+
+
+def run_reference(args):
+    """CPU reference arm: oracle (C restatement of K, bit-exact) on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+    from paper_1911_00675_b200 import datagen
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    full = datagen.config2()
+    sample_sets = _reference_sample(full)
+    sub = full.subset(sample_sets)
+    orc.lib()
+    times = []
+    for step in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        for v in VARIANTS:
+            orc.sketch_csr(v, M, sub.ids, sub.weights, sub.offsets, threads=cores)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+    ms = float(np.mean(times)) * 1e3
+    value = len(VARIANTS) * sub.nelems / (ms / 1e3)
+    sample = (f"{sub.nsets} of {full.nsets} config-2 sets (stratified by size, "
+              f"{sub.nelems} elements) x 7 variants per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64+u64", "data": "synthetic",
+        "config": {"workload": "config2: 10k log-uniform weighted sets, 7 weighted variants, m=1024",
+                   "global_batch": sub.nsets, "m": M},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _reference_sample(full, target_elems=400_000):
+    """Stratified subset: every k-th set in size order, ~target_elems total."""
+    sizes = np.diff(full.offsets)
+    order = np.argsort(sizes, kind="stable")
+    k = max(1, int(np.ceil(sizes.sum() / target_elems)))
+    return np.sort(order[::k])
+
+
+def cpu_baseline_ours_line(full, cores):
+    """cpu_baseline object for our arm's line: the oracle on a bounded sample."""
+    from oracle import oracle as orc
+    sub = full.subset(_reference_sample(full, 200_000))
+    orc.lib()
+    t0 = time.perf_counter()
+    for v in VARIANTS:
+        orc.sketch_csr(v, M, sub.ids, sub.weights, sub.offsets, threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": len(VARIANTS) * sub.nelems / dt, "unit": UNIT, "cores": cores,
+            "kind": "port",
+            "sample": f"{sub.nsets} stratified config-2 sets ({sub.nelems} elements) x 7 variants, "
+                      f"oracle/pmh_oracle.c on {cores} threads"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variants", default=",".join(VARIANTS))
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+
+    from paper_1911_00675_b200 import _lib, datagen
+    from paper_1911_00675_b200.batch import to_device_f64, to_device_i64, to_device_u64
+
+    variants = args.variants.split(",")
+    L = _lib.load()
+    batch = datagen.config2(seed=2 + rank)
+    N, S = batch.nelems, batch.nsets
+    ids = to_device_u64(batch.ids)
+    w = to_device_f64(batch.weights)
+    off = to_device_i64(batch.offsets)
+    sig = torch.empty((S, M), dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    err = ctypes.c_int64(-1)
+    status = torch.empty(2, dtype=torch.int64, device="cuda")
+    _lib.check(L.pmh_status_reset(status.data_ptr(), sp))
+
+    def launch(v):
+        # asynchronous C-ABI entry: no host sync inside the timed region
+        _lib.check(L.pmh_sketch_csr_async(_lib.ALG[v], M, ids.data_ptr(), w.data_ptr(),
+                                          off.data_ptr(), S, sig.data_ptr(), None,
+                                          status.data_ptr(), sp))
+
+    for _ in range(args.warmup):
+        for v in variants:
+            launch(v)
+    torch.cuda.synchronize()
+
+    ev = {v: [] for v in variants}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for _ in range(args.steps):
+            for v in variants:
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                launch(v)
+                b.record(stream)
+                ev[v].append((a, b))
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    _lib.check(L.pmh_status_check(status.data_ptr(), ctypes.byref(err), sp), err.value)
+    ms_total = t_start.elapsed_time(t_end)
+    if world > 1:
+        t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    per_variant_ms = {v: float(np.mean([a.elapsed_time(b) for a, b in ev[v]])) for v in variants}
+    value = world * len(variants) * N / (ms_step / 1e3)
+
+    # ---- e2e: C ABI host entry, pinned host buffers, copies inside timing ----
+    h_ids = torch.from_numpy(batch.ids.view(np.int64)).pin_memory()
+    h_w = torch.from_numpy(batch.weights).pin_memory()
+    h_off = torch.from_numpy(batch.offsets).pin_memory()
+    h_sig = torch.empty((S, M), dtype=torch.int64).pin_memory()
+
+    def e2e_call(v):
+        rc = L.pmh_sketch_csr_host(_lib.ALG[v], M, h_ids.data_ptr(), h_w.data_ptr(),
+                                   h_off.data_ptr(), S, N, h_sig.data_ptr(), None,
+                                   ctypes.byref(err))
+        _lib.check(rc, err.value)
+
+    e2e_s = float("nan")
+    if args.e2e_steps > 0:
+        e2e_call(variants[-1])
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            for v in variants:
+                e2e_call(v)
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = len(variants) * (batch.ids.nbytes + batch.weights.nbytes + batch.offsets.nbytes)
+    d2h = len(variants) * S * M * 8
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    hbm_peak, peak_src = _peaks()
+    dom = max(per_variant_ms, key=per_variant_ms.get)
+    alg_bytes = algorithmic_bytes(N, S, M)
+    achieved = alg_bytes / (per_variant_ms[dom] / 1e3) / 1e9
+    roofline = {
+        "bound": "hbm", "kernel": f"sketch[{dom}]", "achieved": achieved, "peak": hbm_peak,
+        "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+        "peak_source": peak_src,
+        "algorithmic_bytes": alg_bytes,
+        "note": "achieved = SURVEY §8d algorithmic bytes (16 B/elt + 8m B/set + 8 B/set) "
+                "per launch / mean CUDA-event launch time",
+    }
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_ours_line(batch, cores)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64+u64", "data": "synthetic",
+        "config": {"workload": "config2: 10k log-uniform weighted sets, 7 weighted variants, m=1024",
+                   "sets_per_gpu": S, "elements_per_gpu": N, "m": M,
+                   "variants": variants, "l2": "inputs 1.47 GB > 126 MB L2"},
+        "per_variant_ms": per_variant_ms,
+        "per_variant_elems_per_s": {v: N / (t / 1e3) for v, t in per_variant_ms.items()},
+        "e2e": {"value": world * len(variants) * N / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": len(variants) * args.steps,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -79,6 +79,20 @@ int pmh_sketch_csr(int algo, int64_t m, const uint64_t* ids,
                    int64_t nsets, uint64_t* sig_out, int64_t* stats_out,
                    int64_t* err_set, void* stream);
 
+/*
+ * Asynchronous form: enqueue on `stream` without synchronising.  d_status is a
+ * caller-owned DEVICE int64[2] initialised with pmh_status_reset(); device-side
+ * failures (EMPTY / RANDOMNESS) accumulate there and are reported by
+ * pmh_status_check(), which synchronises the stream.  Host-side argument
+ * errors are returned immediately.  pmh_sketch_csr == reset + async + check.
+ */
+int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
+                         const double* weights, const int64_t* offsets,
+                         int64_t nsets, uint64_t* sig_out, int64_t* stats_out,
+                         int64_t* d_status, void* stream);
+int pmh_status_reset(int64_t* d_status, void* stream);
+int pmh_status_check(const int64_t* d_status, int64_t* err_set, void* stream);
+
 /* Same with HOST buffers (pageable or pinned); nelems = offsets[nsets]. */
 int pmh_sketch_csr_host(int algo, int64_t m, const uint64_t* ids,
                         const double* weights, const int64_t* offsets,

@@ -33,7 +33,8 @@ ALG = {
 UNWEIGHTED_IDS = {10, 11, 12, 13, 14, 15, 16, 17, 18}
 
 # every symbol include/pmh.h declares
-EXPORTS = ("pmh_version", "pmh_last_error", "pmh_sketch_csr", "pmh_sketch_csr_host",
+EXPORTS = ("pmh_version", "pmh_last_error", "pmh_sketch_csr", "pmh_sketch_csr_async",
+           "pmh_status_reset", "pmh_status_check", "pmh_sketch_csr_host",
            "pmh_count_equal", "pmh_allpairs_tile", "pmh_bbit")
 
 _lib = None
@@ -64,6 +65,13 @@ def load():
         L.pmh_sketch_csr.argtypes = [ctypes.c_int, _i64, _vp, _vp, _vp, _i64, _vp, _vp,
                                      _i64p, _vp]
         L.pmh_sketch_csr.restype = ctypes.c_int
+        L.pmh_sketch_csr_async.argtypes = [ctypes.c_int, _i64, _vp, _vp, _vp, _i64, _vp, _vp,
+                                           _vp, _vp]
+        L.pmh_sketch_csr_async.restype = ctypes.c_int
+        L.pmh_status_reset.argtypes = [_vp, _vp]
+        L.pmh_status_reset.restype = ctypes.c_int
+        L.pmh_status_check.argtypes = [_vp, _i64p, _vp]
+        L.pmh_status_check.restype = ctypes.c_int
         L.pmh_sketch_csr_host.argtypes = [ctypes.c_int, _i64, _vp, _vp, _vp, _i64, _i64,
                                           _vp, _vp, _i64p]
         L.pmh_sketch_csr_host.restype = ctypes.c_int

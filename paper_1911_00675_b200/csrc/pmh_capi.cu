@@ -18,7 +18,7 @@
 
 #include "../../include/pmh.h"
 #include "pmh_pminhash.cuh"
-#include "pmh_sketch.cuh"
+#include "pmh_kernel.cuh"
 
 using namespace pmh;
 
@@ -41,7 +41,6 @@ int cuda_fail(cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return cuda_fail(_e, #call); \
   } while (0)
 
-constexpr int ERRF_EMPTY = 4;
 
 // ---- constant tables (glibc on the host, uploaded once per device and m) --
 struct DevTables {
@@ -127,9 +126,9 @@ int64_t min_m(int algo) {
 
 template <int F>
 cudaError_t launch_family(const SketchArgs& a, cudaStream_t st) {
-  const int threads = 256;
-  size_t smem = sizeof(Slot) * (size_t)a.m;
-  if (family_uses_fy(F)) smem += (size_t)(threads / 32) * sizeof(int32_t) * (size_t)(a.m + 1);
+  const int threads = SKETCH_THREADS;
+  const size_t smem = sketch_smem_bytes(F, a.m, threads);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(sketch_sets_kernel<F>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -140,9 +139,7 @@ cudaError_t launch_family(const SketchArgs& a, cudaStream_t st) {
 
 template <int C, bool EXPO>
 cudaError_t launch_pmin_c(const PMinArgs& a, cudaStream_t st) {
-  const int tpg = (int)((a.m + C - 1) / C);
-  const int groups = PMIN_THREADS / tpg;
-  const size_t smem = sizeof(Slot) * (size_t)groups * (size_t)a.m;
+  const size_t smem = sizeof(Slot) * (size_t)a.m;
   cudaError_t e = cudaFuncSetAttribute(pminhash_kernel<C, EXPO>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -153,10 +150,21 @@ cudaError_t launch_pmin_c(const PMinArgs& a, cudaStream_t st) {
 
 template <bool EXPO>
 cudaError_t launch_pminhash(const PMinArgs& a, cudaStream_t st) {
-  // C = components per thread: smallest power of two with m/C <= 128
-  // (>= 2 groups of threads per CTA), capped at 32 (registers)
+  if (a.m % PM64_C == 0 && a.m / PM64_C <= PMIN_THREADS) {
+    const size_t smem = sizeof(Slot) * (size_t)a.m;
+    cudaError_t e = cudaFuncSetAttribute(pminhash64_kernel<EXPO>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t grid = a.nsets < 2147483647LL ? a.nsets : 2147483647LL;
+    pminhash64_kernel<EXPO><<<(unsigned)grid, PMIN_THREADS, smem, st>>>(a);
+    return cudaGetLastError();
+  }
+  // C = components per thread: 32 for m >= 1024 (one warp per group at
+  // m = 1024, 8 groups per CTA), else the power of two giving ~32 threads per
+  // group; m <= 256 * 32 required
   int64_t c = 1;
-  while (a.m > 128 * c && c < 32) c *= 2;
+  while (a.m > 32 * c && c < 32) c *= 2;
+  if (a.m > (int64_t)PMIN_THREADS * c) return cudaErrorInvalidValue;
   switch (c) {
     case 1: return launch_pmin_c<1, EXPO>(a, st);
     case 2: return launch_pmin_c<2, EXPO>(a, st);
@@ -175,29 +183,50 @@ int pmh_version(void) { return 100; }
 
 const char* pmh_last_error(void) { return g_last_error.c_str(); }
 
-int pmh_sketch_csr(int algo, int64_t m, const uint64_t* ids,
-                   const double* weights, const int64_t* offsets,
-                   int64_t nsets, uint64_t* sig_out, int64_t* stats_out,
-                   int64_t* err_set, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+int pmh_status_reset(int64_t* d_status, void* stream) {
+  const long long init[2] = {0, 0x7FFFFFFFFFFFFFFFLL};
+  // small pageable copy: the driver stages it, stream-ordered
+  PMH_CUDA(cudaMemcpyAsync(d_status, init, sizeof(init), cudaMemcpyHostToDevice,
+                           (cudaStream_t)stream));
+  return PMH_OK;
+}
+
+int pmh_status_check(const int64_t* d_status, int64_t* err_set, void* stream) {
+  long long h[2] = {0, 0};
+  PMH_CUDA(cudaMemcpyAsync(h, d_status, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  PMH_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   if (err_set) *err_set = -1;
+  if (h[1] != 0x7FFFFFFFFFFFFFFFLL) {
+    if (err_set) *err_set = h[1];
+    if (h[0] & ERRF_RANDOMNESS)
+      return set_error(PMH_ERR_RANDOMNESS, "rejection or coupon loop exceeded its cap in set " +
+                                               std::to_string(h[1]));
+    return set_error(PMH_ERR_EMPTY, "cannot sketch an empty set (set " + std::to_string(h[1]) + ")");
+  }
+  return PMH_OK;
+}
+
+int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
+                         const double* weights, const int64_t* offsets,
+                         int64_t nsets, uint64_t* sig_out, int64_t* stats_out,
+                         int64_t* d_status, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
   const int fam = family_of(algo);
   if (algo != ALG_PMINHASH && algo != ALG_MINHASH && fam == 0)
     return set_error(PMH_ERR_INVALID, "unsupported algorithm id " + std::to_string(algo));
   if (m < min_m(algo))
     return set_error(PMH_ERR_INVALID, "signature size must be >= " + std::to_string(min_m(algo)));
-  if (m > 65536) return set_error(PMH_ERR_INVALID, "signature size must be <= 65536");
+  if (algo != ALG_PMINHASH && algo != ALG_MINHASH &&
+      sketch_smem_bytes(fam, m, SKETCH_THREADS) > 227 * 1024)
+    return set_error(PMH_ERR_INVALID, "signature size too large for the shared-memory slot table");
+  if (m > 65535) return set_error(PMH_ERR_INVALID, "signature size must be <= 65535");
   if (nsets < 0) return set_error(PMH_ERR_INVALID, "negative set count");
   if (nsets == 0) return PMH_OK;
   if (!is_unweighted(algo) && !weights)
     return set_error(PMH_ERR_INVALID, "weighted algorithm requires weights");
-
-  int* d_flags = nullptr;
-  PMH_CUDA(cudaMallocAsync((void**)&d_flags, 16, st));
-  long long* d_err_set = (long long*)((char*)d_flags + 8);
-  const long long init_set = 0x7FFFFFFFFFFFFFFFLL;
-  PMH_CUDA(cudaMemsetAsync(d_flags, 0, 8, st));
-  PMH_CUDA(cudaMemcpyAsync(d_err_set, &init_set, 8, cudaMemcpyHostToDevice, st));
+  if (!d_status) return set_error(PMH_ERR_INVALID, "status buffer required");
+  unsigned long long* flags = reinterpret_cast<unsigned long long*>(d_status);
+  long long* d_err_set = reinterpret_cast<long long*>(d_status + 1);
 
   cudaError_t e;
   if (algo == ALG_PMINHASH || algo == ALG_MINHASH) {
@@ -207,7 +236,7 @@ int pmh_sketch_csr(int algo, int64_t m, const uint64_t* ids,
   } else {
     const Tables* tp = nullptr;
     int rc = get_tables(fam, m, &tp);
-    if (rc) { cudaFreeAsync(d_flags, st); return rc; }
+    if (rc) return rc;
     SketchArgs a{};
     a.ids = ids;
     a.w = is_unweighted(algo) ? nullptr : weights;
@@ -217,7 +246,7 @@ int pmh_sketch_csr(int algo, int64_t m, const uint64_t* ids,
     a.m = m;
     a.sig = sig_out;
     a.stats = stats_out;
-    a.err_flags = d_flags;
+    a.err_flags = flags;
     a.err_set = d_err_set;
     a.T = *tp;
     a.tconst = 4.0;
@@ -230,26 +259,31 @@ int pmh_sketch_csr(int algo, int64_t m, const uint64_t* ids,
       default: e = launch_family<FAM_UW4>(a, st); break;
     }
   }
-  if (e != cudaSuccess) { cudaFreeAsync(d_flags, st); return cuda_fail(e, "kernel launch"); }
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   if (stats_out && !reports_buffer(algo) && algo != ALG_PMINHASH && algo != ALG_MINHASH) {
     // the non-interleaved variants have no buffer (K:334-336): column 1 = 0
     PMH_CUDA(cudaMemset2DAsync(stats_out + 1, 3 * sizeof(int64_t), 0, sizeof(int64_t),
                                (size_t)nsets, st));
   }
-  int h_flags[4] = {0, 0, 0, 0};
-  PMH_CUDA(cudaMemcpyAsync(h_flags, d_flags, 16, cudaMemcpyDeviceToHost, st));
-  PMH_CUDA(cudaFreeAsync(d_flags, st));
-  PMH_CUDA(cudaStreamSynchronize(st));
-  long long bad;
-  memcpy(&bad, &h_flags[2], 8);
-  if (bad != init_set) {
-    if (err_set) *err_set = bad;
-    if (h_flags[0] & ERRF_RANDOMNESS)
-      return set_error(PMH_ERR_RANDOMNESS, "rejection or coupon loop exceeded its cap in set " +
-                                               std::to_string(bad));
-    return set_error(PMH_ERR_EMPTY, "cannot sketch an empty set (set " + std::to_string(bad) + ")");
-  }
   return PMH_OK;
+}
+
+int pmh_sketch_csr(int algo, int64_t m, const uint64_t* ids,
+                   const double* weights, const int64_t* offsets,
+                   int64_t nsets, uint64_t* sig_out, int64_t* stats_out,
+                   int64_t* err_set, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (err_set) *err_set = -1;
+  if (nsets == 0 && m >= min_m(algo)) return PMH_OK;
+  int64_t* d_status = nullptr;
+  PMH_CUDA(cudaMallocAsync((void**)&d_status, 16, st));
+  int rc = pmh_status_reset(d_status, st);
+  if (rc == PMH_OK)
+    rc = pmh_sketch_csr_async(algo, m, ids, weights, offsets, nsets, sig_out, stats_out,
+                              d_status, st);
+  if (rc == PMH_OK) rc = pmh_status_check(d_status, err_set, st);
+  cudaFreeAsync(d_status, st);
+  return rc;
 }
 
 int pmh_sketch_csr_host(int algo, int64_t m, const uint64_t* ids,

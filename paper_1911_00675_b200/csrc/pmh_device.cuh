@@ -56,6 +56,17 @@ struct Stream {
   uint64_t buf;  // buffered bits, LSB first
   uint32_t nb;   // number of buffered bits
   __device__ __forceinline__ void seed(uint64_t id) { s = id; buf = 0; nb = 0; }
+  // position the cursor at absolute bit offset `off` of the stream of `id`
+  __device__ __forceinline__ void seek(uint64_t id, uint64_t off) {
+    s = id + (off >> 6) * GOLDEN;
+    const uint32_t r = (uint32_t)(off & 63);
+    if (r) { const uint64_t w = next_u64(); buf = w >> r; nb = 64 - r; }
+    else { buf = 0; nb = 0; }
+  }
+  // absolute bit offset of the cursor (words generated * 64 - buffered)
+  __device__ __forceinline__ uint64_t pos(uint64_t id) const {
+    return ((s - id) * 0xF1DE83E19937733DULL) * 64ULL - nb;  // (s-id)/GOLDEN: inverse of GOLDEN mod 2^64
+  }
   __device__ __forceinline__ uint64_t next_u64() { s += GOLDEN; return mix64(s); }
   // consumes exactly k bits, 1 <= k <= 63 (K:63-78)
   __device__ __forceinline__ uint64_t next_bits(uint32_t k) {

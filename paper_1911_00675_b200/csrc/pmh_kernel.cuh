@@ -1,0 +1,177 @@
+// pmh_kernel.cuh -- the set-level ProbMinHash kernel (one CTA per set).
+//
+// Per set: slot table + h_max in shared memory; warps pull chunks of
+// elements from a shared counter.  Within a chunk each lane takes one
+// element; elements whose expected point count w * thr is small are run
+// lane-per-element through the reference recurrence (pmh_sketch.cuh, "mode
+// A"); long elements (small sets, heavy weights) and Fisher-Yates elements
+// that outgrow the per-lane sparse map are run warp-cooperatively
+// (pmh_warp.cuh, "mode B").  The final verification max_k h_k <= t makes the
+// threshold guess t exact-safe (retry with a larger t otherwise).
+#pragma once
+#include "pmh_warp.cuh"
+
+namespace pmh {
+
+constexpr double HEAVY_POINTS = 8.0;   // expected points above which mode B runs
+constexpr int SKETCH_THREADS = 256;
+
+__host__ __device__ inline size_t sketch_smem_bytes(int family, int64_t m, int threads) {
+  const int nw = threads / 32;
+  size_t b = sizeof(Slot) * (size_t)m;
+  b += sizeof(WarpScratch) * (size_t)nw;
+  if (family_uses_fy(family)) b += sizeof(uint32_t) * (size_t)(m + 1) * (size_t)nw;
+  return (b + 15) & ~(size_t)15;
+}
+
+// Dynamic shared memory: Slot[m] | WarpScratch[nwarps] | int32 FY[nwarps][m+1]
+template <int F>
+__global__ void __launch_bounds__(SKETCH_THREADS) sketch_sets_kernel(SketchArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned long long s_hmax;
+  __shared__ unsigned int s_filled;
+  __shared__ unsigned int s_next;
+  __shared__ int s_retry;
+  __shared__ double s_red[32];
+  __shared__ long long s_redl[32];
+
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int64_t m = a.m;
+  Slot* slots = reinterpret_cast<Slot*>(smem);
+  WarpScratch* wscr = reinterpret_cast<WarpScratch*>(smem + sizeof(Slot) * m) + wid;
+  uint32_t* fy_dense = reinterpret_cast<uint32_t*>(
+                           smem + sizeof(Slot) * m + sizeof(WarpScratch) * nwarps) +
+                       (size_t)wid * (m + 1);
+  if (family_uses_fy(F)) {  // epoch 0 never matches: the map starts empty
+    for (int64_t p = lane; p <= m; p += 32) fy_dense[p] = 0;
+    if (lane == 0) wscr->epoch = 0;
+  }
+  // mode B needs static point offsets (power-of-two m) unless the family
+  // parses its bit offsets (Fisher-Yates families)
+  const bool warp_ok = family_uses_fy(F) || ((m & (m - 1)) == 0);
+
+  for (int64_t bs = blockIdx.x; bs < a.nsets; bs += gridDim.x) {
+    const int64_t s = a.order ? (int64_t)a.order[bs] : bs;
+    const int64_t off = a.offsets[s];
+    const int64_t n = a.offsets[s + 1] - off;
+    if (n <= 0) {
+      if (threadIdx.x == 0) atomicMin(a.err_set, (long long)s);
+      continue;
+    }
+    const uint64_t* ids = a.ids + off;
+    const double* w = a.w ? a.w + off : nullptr;
+
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+      slots[k].h = EMPTY_H;
+      slots[k].idx = EMPTY_IDX;
+    }
+    double W;
+    if (family_weighted(F) && w) {
+      double part = 0.0;
+      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) part += w[e];
+      W = block_sum(part, s_red);
+    } else {
+      W = (double)n;
+    }
+    if (threadIdx.x == 0) { s_hmax = EMPTY_H; s_filled = 0; }
+
+    SetCtx c;
+    c.slots = slots;
+    c.hmax_bits = &s_hmax;
+    c.filled = &s_filled;
+    c.m = m;
+    c.kbits = bits_for(m);
+    c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
+    c.points = 0; c.updates = 0; c.multi = 0;
+    double tg = (double)m * (log((double)m) + a.tconst) / W;
+    if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
+    bool failed = false;
+    int64_t chunk = (n + 2 * nwarps - 1) / (2 * nwarps);
+    chunk = chunk < 1 ? 1 : (chunk > 32 ? 32 : chunk);
+
+    for (int attempt = 0;; attempt++) {
+      c.tguess = tg;
+      if (threadIdx.x == 0) s_next = 0;
+      __syncthreads();
+      for (;;) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(&s_next, (unsigned)chunk);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if ((int64_t)base >= n) break;
+        const int64_t e = (int64_t)base + lane;
+        const bool active = lane < chunk && e < n;
+        uint64_t id = 0;
+        double winv = 1.0;
+        bool heavy = false;
+        int status = EL_DONE;
+        if (active) {
+          id = ids[e];
+          if (family_weighted(F) && w) winv = 1.0 / w[e];
+          heavy = warp_ok && ctx_thr(c) > HEAVY_POINTS * winv;
+          if (!heavy) {
+            SparseFY fy; fy.reset();
+            status = run_element<F>(c, a.T, fy, e, id, winv);
+          }
+        }
+        if (status == EL_FAIL) failed = true;
+        unsigned hm = __ballot_sync(0xffffffffu, active && (heavy || status == EL_NEED_WARP));
+        while (hm) {
+          const int l = __ffs(hm) - 1;
+          hm &= hm - 1;
+          const int64_t eh = __shfl_sync(0xffffffffu, e, l);
+          const uint64_t idh = __shfl_sync(0xffffffffu, id, l);
+          const double winvh = __shfl_sync(0xffffffffu, winv, l);
+          const int st = warp_element<F>(c, a.T, *wscr, fy_dense, lane, eh, idh, winvh);
+          if (st == EL_FAIL) failed = true;
+          if (lane == 0) c.multi++;
+          __syncwarp();
+        }
+        hmax_refresh_warp(c, lane);
+      }
+      __syncthreads();
+      // verification: every slot non-empty and <= tguess
+      unsigned long long mx = 0;
+      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+        unsigned long long h = slots[k].h;
+        mx = h > mx ? h : mx;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = v > mx ? v : mx;
+      }
+      if (threadIdx.x == 0) s_retry = 0;
+      __syncthreads();
+      if (lane == 0 && __longlong_as_double((long long)mx) > tg) atomicOr(&s_retry, 1);
+      const int any_fail = __syncthreads_or(failed ? 1 : 0);
+      if (any_fail) { failed = true; break; }
+      if (!s_retry) break;
+      tg = attempt >= 2 ? __longlong_as_double(0x7FF0000000000000LL) : tg * 4.0;
+      __syncthreads();
+    }
+    if (failed) {
+      if (threadIdx.x == 0) {
+        atomicOr(a.err_flags, (unsigned long long)ERRF_RANDOMNESS);
+        atomicMin(a.err_set, (long long)s);
+      }
+    }
+    uint64_t* sig = a.sig + (size_t)s * m;
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+      const unsigned long long ix = slots[k].idx;
+      sig[k] = ix < (unsigned long long)n ? ids[ix] : 0ULL;
+    }
+    if (a.stats) {
+      long long pts = block_sum_ll(c.points, s_redl);
+      long long mul = block_sum_ll(c.multi, s_redl);
+      long long upd = block_sum_ll(c.updates, s_redl);
+      if (threadIdx.x == 0) {
+        a.stats[s * 3 + 0] = pts;
+        a.stats[s * 3 + 1] = mul;
+        a.stats[s * 3 + 2] = upd;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace pmh

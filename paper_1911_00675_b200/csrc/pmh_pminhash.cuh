@@ -33,22 +33,33 @@ struct PMinArgs {
 constexpr int PMIN_THREADS = 256;
 constexpr int PMIN_CHUNK = 256;
 
-// C components per thread; words of thread's bit range are generated once per
-// element with an incremental splitmix state.
-// EXPO = true: P-MinHash h = winv * Exp(1) (K:284-300);
-// EXPO = false: MinHash h = U (K:768-781), unit weights.
+// Thread (g, t) owns components [t*C, t*C + C) and walks elements g, g+G, ...
+// of its set in increasing order; G groups of ceil(m/C) threads per CTA.
+//
+// Hot loop (almost every draw is rejected once the minima are small): with
+// T_t = max of the thread's C running minima and sw(e) = w_e * 2^53 * (1 +
+// 2^-40), any draw with raw bits b >= Tb = ceil(T_t * sw(e)) + 1 satisfies
+// fl(winv * E(b)) >= winv * b * 2^-53 * (1 - 2^-51) > T_t >= hmin_q, so it
+// cannot lower any of the thread's minima: the per-draw work is integer
+// only (splitmix64 words, a funnel-shift extraction and one 64-bit compare).
+// Draws below Tb take the exact path: the reference's
+// h = winv * (-log1p(-U)) with glibc-exact log1p and strict `<`.
+//
+// EXPO = true: P-MinHash (K:284-300); EXPO = false: MinHash h = U (K:768-781).
 template <int C, bool EXPO>
 __global__ void __launch_bounds__(PMIN_THREADS) pminhash_kernel(PMinArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint64_t s_id[PMIN_CHUNK];
   __shared__ double s_winv[PMIN_CHUNK];
+  __shared__ double s_sw[PMIN_CHUNK];
   const int64_t m = a.m;
   const int tpg = (int)((m + C - 1) / C);          // threads per group
   const int groups = PMIN_THREADS / tpg;           // >= 1 (host guarantees)
   const int g = threadIdx.x / tpg, t = threadIdx.x % tpg;
   const bool active = g < groups;
   const int64_t k0 = (int64_t)t * C;
-  Slot* part = reinterpret_cast<Slot*>(smem);      // [groups][m]
+  Slot* table = reinterpret_cast<Slot*>(smem);     // [m] merged minima
+  const double two53m = 9007199254740992.0 * 1.0000000000009095;  // 2^53 (1 + 2^-40)
 
   for (int64_t bs = blockIdx.x; bs < a.nsets; bs += gridDim.x) {
     const int64_t s = a.order ? (int64_t)a.order[bs] : bs;
@@ -58,24 +69,37 @@ __global__ void __launch_bounds__(PMIN_THREADS) pminhash_kernel(PMinArgs a) {
       if (threadIdx.x == 0) atomicMin(a.err_set, (long long)s);
       continue;
     }
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+      table[k].h = EMPTY_H;
+      table[k].idx = EMPTY_IDX;
+    }
     double hmin[C];
-    unsigned long long arg[C];
+    uint32_t arg[C];
 #pragma unroll
-    for (int q = 0; q < C; q++) { hmin[q] = __longlong_as_double(0x7FF0000000000000LL); arg[q] = EMPTY_IDX; }
+    for (int q = 0; q < C; q++) { hmin[q] = __longlong_as_double(0x7FF0000000000000LL); arg[q] = 0xFFFFFFFFu; }
+    double tmax = __longlong_as_double(0x7FF0000000000000LL);   // max_q hmin[q]
 
     for (int64_t c0 = 0; c0 < n; c0 += PMIN_CHUNK) {
       const int64_t cn = n - c0 < PMIN_CHUNK ? n - c0 : PMIN_CHUNK;
       __syncthreads();
       if (threadIdx.x < cn) {
         s_id[threadIdx.x] = a.ids[off + c0 + threadIdx.x];
-        s_winv[threadIdx.x] = (EXPO && a.w) ? 1.0 / a.w[off + c0 + threadIdx.x] : 1.0;
+        if (EXPO) {
+          const double w = a.w ? a.w[off + c0 + threadIdx.x] : 1.0;
+          s_winv[threadIdx.x] = 1.0 / w;
+          s_sw[threadIdx.x] = w * two53m;
+        } else {
+          s_sw[threadIdx.x] = two53m;
+        }
       }
       __syncthreads();
       if (!active) continue;
       for (int64_t le = g; le < cn; le += groups) {
         const uint64_t id = s_id[le];
-        const double winv = s_winv[le];
-        const uint64_t e = (uint64_t)(c0 + le);
+        const uint32_t e = (uint32_t)(c0 + le);
+        // integer rejection threshold for this element
+        const double tb = tmax * s_sw[le];
+        const uint64_t Tb = tb < 9007199254740992.0 ? (uint64_t)tb + 1ULL : (1ULL << 53);
         uint64_t bitpos = 53ULL * (uint64_t)k0;
         uint64_t wi = bitpos >> 6;                  // 0-based word index
         uint32_t sh = (uint32_t)(bitpos & 63);
@@ -83,19 +107,23 @@ __global__ void __launch_bounds__(PMIN_THREADS) pminhash_kernel(PMinArgs a) {
         uint64_t lo = mix64(st);
         st += GOLDEN;
         uint64_t hi = mix64(st);
+        bool changed = false;
 #pragma unroll
         for (int q = 0; q < C; q++) {
           if (k0 + q < m) {
             uint64_t b = sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
             b &= (1ULL << 53) - 1ULL;
-            if constexpr (EXPO) {
-              if (!(exp1_scaled_lower_bound(winv, b) > hmin[q])) {
-                const double h = winv * exp1_from_bits(b);
-                if (h < hmin[q]) { hmin[q] = h; arg[q] = e; }
+            if (b < Tb) {
+              if constexpr (EXPO) {
+                const double winv = s_winv[le];
+                if (!(exp1_scaled_lower_bound(winv, b) > hmin[q])) {
+                  const double h = winv * exp1_from_bits(b);
+                  if (h < hmin[q]) { hmin[q] = h; arg[q] = e; changed = true; }
+                }
+              } else {
+                const double h = (double)b * INV53;
+                if (h < hmin[q]) { hmin[q] = h; arg[q] = e; changed = true; }
               }
-            } else {
-              const double h = (double)b * INV53;
-              if (h < hmin[q]) { hmin[q] = h; arg[q] = e; }
             }
           }
           sh += 53;
@@ -105,27 +133,27 @@ __global__ void __launch_bounds__(PMIN_THREADS) pminhash_kernel(PMinArgs a) {
             if (q + 1 < C) { st += GOLDEN; hi = mix64(st); }
           }
         }
+        if (changed) {
+          double mx = 0.0;
+#pragma unroll
+          for (int q = 0; q < C; q++)
+            if (k0 + q < m) mx = hmin[q] > mx ? hmin[q] : mx;
+          tmax = mx;
+        }
       }
     }
-    // merge groups lexicographically on (h, index)
+    // merge the groups' partial minima lexicographically on (h, index)
     __syncthreads();
     if (active) {
 #pragma unroll
-      for (int q = 0; q < C; q++) {
-        if (k0 + q < m) {
-          part[(size_t)g * m + k0 + q].h = dbl_bits(hmin[q]);
-          part[(size_t)g * m + k0 + q].idx = arg[q];
-        }
-      }
+      for (int q = 0; q < C; q++)
+        if (k0 + q < m && arg[q] != 0xFFFFFFFFu)
+          slot_offer(&table[k0 + q], hmin[q], (unsigned long long)arg[q]);
     }
     __syncthreads();
     uint64_t* sig = a.sig + (size_t)s * m;
     for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-      unsigned long long bh = part[k].h, bi = part[k].idx;
-      for (int gg = 1; gg < groups; gg++) {
-        const unsigned long long h = part[(size_t)gg * m + k].h, ix = part[(size_t)gg * m + k].idx;
-        if (h < bh || (h == bh && ix < bi)) { bh = h; bi = ix; }
-      }
+      const unsigned long long bi = table[k].idx;
       sig[k] = bi < (unsigned long long)n ? a.ids[off + bi] : 0ULL;
     }
     if (a.stats && threadIdx.x == 0) {
@@ -133,6 +161,139 @@ __global__ void __launch_bounds__(PMIN_THREADS) pminhash_kernel(PMinArgs a) {
       a.stats[s * 3 + 1] = 0;
       a.stats[s * 3 + 2] = 0;
     }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Static-schedule variant for m % 64 == 0 (every configuration): thread t of
+// a 16-lane... group owns components [64t, 64t + 64), whose 64 * 53 = 3392 bits
+// are exactly words 53t .. 53t + 52 of each element's stream, so every bit
+// extraction below has a compile-time shift.  The hot loop keeps only the
+// TOP 32 bits of each draw: b < Tb implies (b >> 21) <= ((Tb - 1) >> 21), so
+// testing top32 <= Tb_hi flags a superset of the candidates (false positives
+// only on top-bit ties, probability 2^-32).  Minima live in ONE shared slot
+// table per CTA (128-bit CAS, lexicographic (h, index)); every group of
+// threads refreshes its rejection threshold tmax from that table, so all
+// groups prune with everyone's minima.
+// ---------------------------------------------------------------------------
+constexpr int PM64_C = 64;
+
+// exact path for the flagged draws of one element (rare)
+template <bool EXPO>
+__device__ __noinline__ void pm64_candidates(uint64_t cand, uint64_t id, double winv, uint32_t e,
+                                             int64_t k0, Slot* table) {
+  while (cand) {
+    const int q = __ffsll((long long)cand) - 1;
+    cand &= cand - 1;
+    const uint64_t bitpos = 53ULL * (uint64_t)(k0 + q);
+    const uint64_t wi = bitpos >> 6;
+    const uint32_t sh = (uint32_t)(bitpos & 63);
+    const uint64_t lo = stream_word(id, wi + 1);
+    uint64_t b = lo >> sh;
+    if (sh > 11) b |= stream_word(id, wi + 2) << (64 - sh);
+    b &= (1ULL << 53) - 1ULL;
+    Slot* sl = &table[k0 + q];
+    const double cur = __longlong_as_double((long long)*(volatile unsigned long long*)&sl->h);
+    double h;
+    if constexpr (EXPO) {
+      if (exp1_scaled_lower_bound(winv, b) > cur) continue;
+      h = winv * exp1_from_bits(b);
+    } else {
+      h = (double)b * INV53;
+    }
+    if (h <= cur) slot_offer(sl, h, (unsigned long long)e);
+  }
+}
+
+__device__ __forceinline__ double pm64_tmax(const Slot* table, int64_t k0) {
+  unsigned long long mx = 0;
+#pragma unroll 8
+  for (int q = 0; q < PM64_C; q++) {
+    const unsigned long long h = *(volatile const unsigned long long*)&table[k0 + q].h;
+    mx = h > mx ? h : mx;
+  }
+  return __longlong_as_double((long long)mx);
+}
+
+template <bool EXPO>
+__global__ void __launch_bounds__(PMIN_THREADS) pminhash64_kernel(PMinArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint64_t s_id[PMIN_CHUNK];
+  __shared__ double s_winv[PMIN_CHUNK];
+  __shared__ double s_sw[PMIN_CHUNK];
+  const int64_t m = a.m;
+  const int tpg = (int)(m / PM64_C);               // threads per group
+  const int groups = PMIN_THREADS / tpg;
+  const int g = threadIdx.x / tpg, t = threadIdx.x % tpg;
+  const bool active = g < groups;
+  const int64_t k0 = (int64_t)t * PM64_C;
+  Slot* table = reinterpret_cast<Slot*>(smem);
+  const double two53m = 9007199254740992.0 * 1.0000000000009095;  // 2^53 (1 + 2^-40)
+  const uint64_t wbase = 53ULL * (uint64_t)t + 1ULL;                // first word (1-based)
+
+  for (int64_t bs = blockIdx.x; bs < a.nsets; bs += gridDim.x) {
+    const int64_t s = a.order ? (int64_t)a.order[bs] : bs;
+    const int64_t off = a.offsets[s];
+    const int64_t n = a.offsets[s + 1] - off;
+    if (n <= 0) {
+      if (threadIdx.x == 0) atomicMin(a.err_set, (long long)s);
+      continue;
+    }
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+      table[k].h = EMPTY_H;
+      table[k].idx = EMPTY_IDX;
+    }
+    double tmax = __longlong_as_double(0x7FF0000000000000LL);
+    int since = 0;
+    for (int64_t c0 = 0; c0 < n; c0 += PMIN_CHUNK) {
+      const int64_t cn = n - c0 < PMIN_CHUNK ? n - c0 : PMIN_CHUNK;
+      __syncthreads();
+      if (threadIdx.x < cn) {
+        s_id[threadIdx.x] = a.ids[off + c0 + threadIdx.x];
+        if (EXPO) {
+          const double w = a.w ? a.w[off + c0 + threadIdx.x] : 1.0;
+          s_winv[threadIdx.x] = 1.0 / w;
+          s_sw[threadIdx.x] = w * two53m;
+        } else {
+          s_winv[threadIdx.x] = 1.0;
+          s_sw[threadIdx.x] = two53m;
+        }
+      }
+      __syncthreads();
+      if (!active) continue;
+      for (int64_t le = g; le < cn; le += groups) {
+        const uint64_t id = s_id[le];
+        const double tb = tmax * s_sw[le];
+        // b < Tb  =>  b >> 21 <= (Tb - 1) >> 21 ; Tb = floor(tb) + 1
+        const uint32_t tbh = tb < 9007199254740992.0 ? (uint32_t)((uint64_t)tb >> 21)
+                                                      : 0xFFFFFFFFu;
+        uint64_t st = id + wbase * GOLDEN;
+        uint32_t c_lo = 0, c_hi = 0;
+#include "pm64_body.inc"
+        const uint64_t cand = ((uint64_t)c_hi << 32) | c_lo;
+        // candidates are cheap (1-2 stream words + a compare against the
+        // slot's own minimum); the threshold refresh (64 shared loads) is
+        // periodic -- a stale, larger tmax only admits more candidates
+        if (cand) pm64_candidates<EXPO>(cand, id, s_winv[le], (uint32_t)(c0 + le), k0, table);
+        if (++since >= 16 || (cand && !(tmax < 1e300))) {
+          tmax = pm64_tmax(table, k0);
+          since = 0;
+        }
+      }
+    }
+    __syncthreads();
+    uint64_t* sig = a.sig + (size_t)s * m;
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+      const unsigned long long bi = table[k].idx;
+      sig[k] = bi < (unsigned long long)n ? a.ids[off + bi] : 0ULL;
+    }
+    if (a.stats && threadIdx.x == 0) {
+      a.stats[s * 3 + 0] = n * m;
+      a.stats[s * 3 + 1] = 0;
+      a.stats[s * 3 + 2] = 0;
+    }
+    __syncthreads();
   }
 }
 

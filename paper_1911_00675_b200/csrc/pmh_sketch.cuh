@@ -100,7 +100,7 @@ __device__ __forceinline__ void hmax_refresh_warp(SetCtx& c, int lane) {
 // Lazy Fisher-Yates (K:222-235).  Positions/values are 1-based; an absent
 // entry means perm[p] == p.
 // ---------------------------------------------------------------------------
-constexpr int SPARSE_FY_CAP = 8;
+constexpr int SPARSE_FY_CAP = 12;
 
 struct SparseFY {
   int32_t pos[SPARSE_FY_CAP];
@@ -341,7 +341,7 @@ struct SketchArgs {
   int64_t m;
   uint64_t* sig;            // [nsets, m]
   int64_t* stats;           // [nsets, 3] or nullptr
-  int* err_flags;           // device, OR of ERRF_*
+  unsigned long long* err_flags;  // device, OR of ERRF_*
   long long* err_set;       // device, min failing set index
   Tables T;
   double tconst;            // threshold-guess constant (ln m + tconst)
@@ -375,145 +375,6 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
   }
   __syncthreads();
   return red[0];
-}
-
-// Dynamic shared memory layout: Slot[m] | int32 FY[nwarps][m+1] (FY families)
-template <int F>
-__global__ void __launch_bounds__(256) sketch_sets_kernel(SketchArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ unsigned long long s_hmax;
-  __shared__ unsigned int s_filled;
-  __shared__ unsigned int s_next;
-  __shared__ int s_retry;
-  __shared__ double s_red[32];
-  __shared__ long long s_redl[32];
-
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
-  const int64_t m = a.m;
-  Slot* slots = reinterpret_cast<Slot*>(smem);
-  int32_t* fy_dense = reinterpret_cast<int32_t*>(smem + sizeof(Slot) * m) +
-                      (size_t)wid * (m + 1);
-
-  for (int64_t bs = blockIdx.x; bs < a.nsets; bs += gridDim.x) {
-    const int64_t s = a.order ? (int64_t)a.order[bs] : bs;
-    const int64_t off = a.offsets[s];
-    const int64_t n = a.offsets[s + 1] - off;
-    if (n <= 0) {
-      if (threadIdx.x == 0) atomicMin(a.err_set, (long long)s);
-      continue;
-    }
-    const uint64_t* ids = a.ids + off;
-    const double* w = a.w ? a.w + off : nullptr;
-
-    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-      slots[k].h = EMPTY_H;
-      slots[k].idx = EMPTY_IDX;
-    }
-    // W = sum of weights (unit weights: n)
-    double W;
-    if (family_weighted(F) && w) {
-      double part = 0.0;
-      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) part += w[e];
-      W = block_sum(part, s_red);
-    } else {
-      W = (double)n;
-    }
-    if (threadIdx.x == 0) { s_hmax = EMPTY_H; s_filled = 0; }
-
-    SetCtx c;
-    c.slots = slots;
-    c.hmax_bits = &s_hmax;
-    c.filled = &s_filled;
-    c.m = m;
-    c.kbits = bits_for(m);
-    c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
-    c.points = 0; c.updates = 0; c.multi = 0;
-    double tg = (double)m * (log((double)m) + a.tconst) / W;
-    if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
-    bool failed = false;
-
-    for (int attempt = 0;; attempt++) {
-      c.tguess = tg;
-      if (threadIdx.x == 0) s_next = 0;
-      __syncthreads();
-      for (;;) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(&s_next, 32u);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if ((int64_t)base >= n) break;
-        const int64_t e = (int64_t)base + lane;
-        int status = EL_DONE;
-        if (e < n) {
-          const uint64_t id = ids[e];
-          const double winv = (family_weighted(F) && w) ? 1.0 / w[e] : 1.0;
-          SparseFY fy; fy.reset();
-          status = run_element<F>(c, a.T, fy, e, id, winv);
-        }
-        if (status == EL_FAIL) failed = true;
-        if constexpr (family_uses_fy(F)) {
-          unsigned heavy = __ballot_sync(0xffffffffu, status == EL_NEED_WARP);
-          while (heavy) {
-            const int l = __ffs(heavy) - 1;
-            heavy &= heavy - 1;
-            const int64_t eh = __shfl_sync(0xffffffffu, e, l);
-            for (int64_t p = lane; p <= m; p += 32) fy_dense[p] = 0;
-            __syncwarp();
-            if (lane == 0) {
-              DenseFY fy{fy_dense};
-              const double winv = (family_weighted(F) && w) ? 1.0 / w[eh] : 1.0;
-              int st = run_element<F>(c, a.T, fy, eh, ids[eh], winv);
-              if (st != EL_DONE) failed = true;
-            }
-            __syncwarp();
-          }
-        }
-        hmax_refresh_warp(c, lane);
-      }
-      __syncthreads();
-      // verification: every slot non-empty and <= tguess
-      unsigned long long mx = 0;
-      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-        unsigned long long h = slots[k].h;
-        mx = h > mx ? h : mx;
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
-        mx = v > mx ? v : mx;
-      }
-      if (threadIdx.x == 0) s_retry = 0;
-      __syncthreads();
-      if (lane == 0 && __longlong_as_double((long long)mx) > tg) atomicOr(&s_retry, 1);
-      const int any_fail = __syncthreads_or(failed ? 1 : 0);
-      if (any_fail) { failed = true; break; }
-      if (!s_retry) break;
-      tg = attempt >= 2 ? __longlong_as_double(0x7FF0000000000000LL) : tg * 4.0;
-      __syncthreads();
-    }
-    if (failed) {
-      if (threadIdx.x == 0) {
-        atomicOr(a.err_flags, ERRF_RANDOMNESS);
-        atomicMin(a.err_set, (long long)s);
-      }
-    }
-    // output
-    uint64_t* sig = a.sig + (size_t)s * m;
-    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-      const unsigned long long ix = slots[k].idx;
-      sig[k] = ix < (unsigned long long)n ? ids[ix] : 0ULL;
-    }
-    if (a.stats) {
-      long long pts = block_sum_ll(c.points, s_redl);
-      long long mul = block_sum_ll(c.multi, s_redl);
-      long long upd = block_sum_ll(c.updates, s_redl);
-      if (threadIdx.x == 0) {
-        a.stats[s * 3 + 0] = pts;
-        a.stats[s * 3 + 1] = mul;
-        a.stats[s * 3 + 2] = upd;
-      }
-    }
-    __syncthreads();
-  }
 }
 
 }  // namespace pmh

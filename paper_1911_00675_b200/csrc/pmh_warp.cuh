@@ -1,0 +1,323 @@
+// pmh_warp.cuh -- warp-cooperative ("lane = point") element processing.
+//
+// An element whose point sequence is long (small sets: the coupon-collector
+// phase needs ~m(ln m + c) points per set, SURVEY.md §7 hard parts) is
+// processed by a whole warp in batches of up to 32 consecutive points:
+//   * the 32 stream words covering the batch are generated once, one mix64
+//     per lane, into a per-warp shared-memory window (2048 bits);
+//   * point bit offsets are static for labels with replacement and power-of-
+//     two m (53 + log2 m bits per point, K:97-110 never rejects), so lanes
+//     decode their point directly; TruncExp's fast path (K:130-132) is
+//     speculated and the first slow-path lane ends the batch after finishing
+//     its draw sequentially;
+//   * labels without replacement (PMH2/PMH4/uw4, K:222-235) have data-
+//     dependent widths: lane 0 parses the batch's bit offsets and runs the
+//     lazy Fisher-Yates steps on a dense per-warp shared map, then all lanes
+//     evaluate the floating-point work in parallel;
+//   * PMH1/PMH2's running sum x_i = fl(x_{i-1} + d_i) is an ordered fold: lane
+//     p adds d_0..d_p in order, which is exactly the reference's sequence of
+//     roundings (K:328, K:440);
+//   * points are valid while x <= thr (x is increasing along an element); the
+//     valid prefix is offered to the slot table.
+#pragma once
+#include "pmh_sketch.cuh"
+
+namespace pmh {
+
+constexpr uint32_t WIN_BITS = 2048;  // 32 words
+
+struct WarpScratch {
+  uint64_t words[33];   // window (+1 guard word)
+  uint32_t eoff[32];    // window-relative bit offset of each point's first draw
+  int32_t lab[32];      // 1-based labels
+  double tval[32];      // TruncExp values (PMH4 parse), NaN => exponential draw
+  uint32_t q;           // points parsed
+  uint32_t flags;       // bit0: batch ended by a slow path; bit1: fail
+  uint64_t next_off;    // absolute bit offset after the batch
+  uint32_t epoch;       // Fisher-Yates map epoch (one per warp-processed element)
+  uint32_t pad;
+};
+
+// Dense per-warp Fisher-Yates map with O(1) reset: entry = epoch << 16 | value
+// (the versioned lazy permutation of K:222-235 / lazyperm.py, one epoch per
+// element).  Requires m < 65536.
+struct EpochFY {
+  uint32_t* a;
+  uint32_t ep;
+  __device__ __forceinline__ int32_t get(int32_t p) const {
+    const uint32_t v = a[p];
+    return (v >> 16) == ep ? (int32_t)(v & 0xffffu) : p;
+  }
+  __device__ __forceinline__ void set(int32_t p, int32_t v) { a[p] = (ep << 16) | (uint32_t)v; }
+};
+
+__device__ __forceinline__ uint64_t win_bits(const uint64_t* w, uint32_t rel, uint32_t k) {
+  const uint32_t i = rel >> 6, sh = rel & 63;
+  uint64_t v = w[i] >> sh;
+  if (sh && sh + k > 64) v |= w[i + 1] << (64 - sh);
+  return k == 64 ? v : (v & ((1ULL << k) - 1ULL));
+}
+
+__device__ __forceinline__ void win_load(WarpScratch& ws, uint64_t id, uint64_t wb, int lane) {
+  ws.words[lane] = stream_word(id, wb + 1 + (uint64_t)lane);
+  if (lane == 0) ws.words[32] = stream_word(id, wb + 33);
+  __syncwarp();
+}
+
+// offer with a refresh trigger instead of an inline serial recompute
+__device__ __forceinline__ bool offer_trig(SetCtx& c, int64_t k0, double x, int64_t e) {
+  unsigned long long prev = slot_offer(&c.slots[k0], x, (unsigned long long)e);
+  if (prev == ~0ULL) return false;
+  c.updates++;
+  if (prev == EMPTY_H) {
+    unsigned f = atomicAdd(c.filled, 1u) + 1u;
+    return f == (unsigned)c.m;
+  }
+  return prev >= *(volatile unsigned long long*)c.hmax_bits;
+}
+
+__device__ __forceinline__ double warp_thr(const SetCtx& c) {
+  return __shfl_sync(0xffffffffu, ctx_thr(c), 0);
+}
+
+// inclusive ordered fold: lane p returns fl(...fl(fl(x0 + d_0) + d_1)... + d_p)
+__device__ __forceinline__ double ordered_fold(double x0, double d, int lane, uint32_t q) {
+  double acc = x0;
+  for (uint32_t j = 0; j < q; j++) {
+    const double v = __shfl_sync(0xffffffffu, d, j);
+    if ((int)j <= lane) acc = acc + v;
+  }
+  return acc;
+}
+
+// ---- labels with replacement, power-of-two m: PMH1, PMH3, uw3 -------------
+
+// F = FAM_PMH1 | FAM_PMH3 | FAM_UW3
+template <int F>
+__device__ int warp_el_static(SetCtx& c, const Tables& T, WarpScratch& ws, int lane,
+                              int64_t e, uint64_t id, double winv) {
+  const uint32_t kb = c.kbits;
+  const uint32_t P = 53 + kb;
+  uint64_t off = 0;     // absolute bit offset of the next point
+  int64_t i = 1;        // next point index (1-based)
+  double x = 0.0;       // PMH1 running sum
+  for (;;) {
+    const uint64_t wb = off >> 6;
+    win_load(ws, id, wb, lane);
+    const uint32_t rel0 = (uint32_t)(off - (wb << 6));
+    uint32_t q = (WIN_BITS - rel0) / P;
+    q = q > 32 ? 32 : q;
+    const double thr = warp_thr(c);
+    const int64_t pt = i + lane;
+    const bool in = (uint32_t)lane < q;
+    uint64_t u = 0;
+    int32_t lab = 0;
+    if (in) {
+      const uint32_t ro = rel0 + (uint32_t)lane * P;
+      u = win_bits(ws.words, ro, 53);
+      lab = (int32_t)win_bits(ws.words, ro + 53, kb) + 1;
+    }
+    double xv = 0.0;
+    uint32_t ncand = q;
+    bool had_slow = false;
+    if constexpr (F == FAM_PMH1) {
+      const double d = in ? winv * exp1_from_bits(u) : 0.0;
+      xv = ordered_fold(x, d, lane, q);
+    } else if constexpr (F == FAM_UW3) {
+      const double U = (double)u * INV53;
+      xv = pt == 1 ? U : ((double)pt - 1.0) + U;
+    } else {  // PMH3: speculate on TruncExp's fast path
+      double t = T.c3.c1 * ((double)u * INV53);
+      const unsigned slow = __ballot_sync(0xffffffffu, in && !(t < 1.0));
+      if (slow) {
+        const int f = __ffs(slow) - 1;
+        ncand = (uint32_t)f + 1;
+        had_slow = true;
+        if (lane == f) {
+          Stream st;
+          st.seek(id, off + (uint64_t)f * P + 53);
+          bool fail = false;
+          t = trunc_exp_slow(st, T.c3, &fail);
+          lab = (int32_t)st.next_bits(kb) + 1;
+          ws.next_off = st.pos(id);
+          ws.flags = fail ? 2u : 0u;
+        }
+        __syncwarp();
+        if (ws.flags & 2u) return EL_FAIL;
+      }
+      xv = pt == 1 ? winv * t : winv * ((double)pt - 1.0) + winv * t;
+    }
+    const bool cand = (uint32_t)lane < ncand;
+    const bool valid = cand && xv <= thr;
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    const bool trig = valid ? offer_trig(c, lab - 1, xv, e) : false;
+    if (__any_sync(0xffffffffu, trig)) hmax_refresh_warp(c, lane);
+    const uint32_t nv = __popc(vm);
+    if (lane == 0) c.points += nv + (nv < ncand ? 1 : 0);
+    if (nv < ncand) return EL_DONE;
+    i += ncand;
+    if (i > c.cap) return EL_FAIL;
+    if constexpr (F == FAM_PMH1) x = __shfl_sync(0xffffffffu, xv, ncand - 1);
+    if (had_slow) off = ws.next_off;
+    else off += (uint64_t)ncand * P;
+    __syncwarp();
+  }
+}
+
+// ---- labels without replacement: PMH2, PMH4, uw4 -------------------------
+
+// Lane 0 parses up to 32 points of the window: bit offsets, rejection draws
+// of the Fisher-Yates indices (uniform_int(m-i+1), K:225), the dense FY map
+// updates, and (PMH4) the TruncExp fast-path test / slow path.
+template <int F>
+__device__ void parse_fy_batch(SetCtx& c, const Tables& T, WarpScratch& ws, EpochFY fy,
+                               uint64_t id, uint64_t off, int64_t i0) {
+  const int64_t m = c.m;
+  const uint64_t wb = off >> 6;
+  uint32_t cur = (uint32_t)(off - (wb << 6));
+  uint32_t q = 0;
+  ws.flags = 0;
+  while (q < 32) {
+    const int64_t pt = i0 + q;
+    if (pt > m) break;
+    if (cur + 53 > WIN_BITS) break;
+    const uint32_t eo = cur;
+    uint32_t c2 = cur + 53;
+    double tv = __longlong_as_double(0x7FF8000000000000LL);  // NaN: Exp(1) draw
+    bool slow = false;
+    Stream st;
+    if (F == FAM_PMH4 && pt < m) {
+      const TruncExpConsts& cc = T.c4[pt];
+      const double t = cc.c1 * ((double)win_bits(ws.words, eo, 53) * INV53);
+      if (t < 1.0) {
+        tv = t;
+      } else {
+        st.seek(id, (wb << 6) + eo + 53);
+        bool fail = false;
+        tv = trunc_exp_slow(st, cc, &fail);
+        if (fail) { ws.flags = 2u; break; }
+        slow = true;
+      }
+    } else if (F == FAM_UW4) {
+      tv = (double)win_bits(ws.words, eo, 53) * INV53;  // the uniform itself
+    }
+    // Fisher-Yates index r = uniform_int(m - pt + 1)
+    const int64_t R = m - pt + 1;
+    int64_t r = 0;
+    if (R > 1) {
+      const uint32_t kb = bits_for(R);
+      if (slow) {
+        r = uniform_int_masked(st, (uint64_t)R, kb);
+        if (r < 0) { ws.flags = 2u; break; }
+      } else {
+        int rounds = 0;
+        bool fits = true;
+        for (;;) {
+          if (c2 + kb > WIN_BITS) { fits = false; break; }
+          const uint64_t v = win_bits(ws.words, c2, kb);
+          c2 += kb;
+          if (v < (uint64_t)R) { r = (int64_t)v; break; }
+          if (++rounds > REJECT_CAP) { ws.flags = 2u; break; }
+        }
+        if (ws.flags & 2u) break;
+        if (!fits) {
+          if (q > 0) break;
+          // the first point of the batch does not fit: finish it sequentially
+          st.seek(id, (wb << 6) + eo + 53);
+          r = uniform_int_masked(st, (uint64_t)R, kb);
+          if (r < 0) { ws.flags = 2u; break; }
+          slow = true;
+        }
+      }
+    }
+    const int32_t j = (int32_t)(pt + r);
+    const int32_t kj = fy.get(j);
+    fy.set(j, fy.get((int32_t)pt));
+    ws.lab[q] = kj;
+    ws.eoff[q] = eo;
+    ws.tval[q] = tv;
+    q++;
+    if (slow) {
+      ws.flags = 1u;
+      ws.next_off = st.pos(id);
+      break;
+    }
+    cur = c2;
+  }
+  ws.q = q;
+  if (!(ws.flags & 1u)) ws.next_off = (wb << 6) + cur;
+}
+
+template <int F>
+__device__ int warp_el_fy(SetCtx& c, const Tables& T, WarpScratch& ws, uint32_t* fy, int lane,
+                          int64_t e, uint64_t id, double winv) {
+  const int64_t m = c.m;
+  uint32_t ep = ws.epoch + 1;
+  if (ep >= 0x10000u) {  // epoch wrap: clear the map once every 65535 elements
+    for (int64_t p = lane; p <= m; p += 32) fy[p] = 0;
+    ep = 1;
+  }
+  __syncwarp();
+  if (lane == 0) ws.epoch = ep;
+  EpochFY efy{fy, ep};
+  uint64_t off = 0;
+  int64_t i = 1;
+  double x = 0.0;
+  for (;;) {
+    const uint64_t wb = off >> 6;
+    win_load(ws, id, wb, lane);
+    if (lane == 0) parse_fy_batch<F>(c, T, ws, efy, id, off, i);
+    __syncwarp();
+    if (ws.flags & 2u) return EL_FAIL;
+    const uint32_t q = ws.q;
+    const double thr = warp_thr(c);
+    const int64_t pt = i + lane;
+    const bool in = (uint32_t)lane < q;
+    double xv = 0.0;
+    if constexpr (F == FAM_PMH2) {
+      double d = 0.0;
+      if (in) {
+        const double E = exp1_from_bits(win_bits(ws.words, ws.eoff[lane], 53));
+        d = pt == 1 ? winv * E : (winv * __ldg(&T.beta[pt])) * E;
+      }
+      xv = ordered_fold(x, d, lane, q);
+    } else if constexpr (F == FAM_PMH4) {
+      if (in) {
+        if (pt == 1) {
+          xv = winv * ws.tval[0];
+        } else if (pt < m) {
+          xv = winv * (__ldg(&T.gam[pt - 1]) + __ldg(&T.dgam[pt]) * ws.tval[lane]);
+        } else {
+          const double E = exp1_from_bits(win_bits(ws.words, ws.eoff[lane], 53));
+          xv = winv * (__ldg(&T.gam[m - 1]) + T.delta * E);
+        }
+      }
+    } else {  // uw4
+      if (in) xv = pt == 1 ? ws.tval[lane] : ((double)pt - 1.0) + ws.tval[lane];
+    }
+    const bool valid = in && xv <= thr;
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    const bool trig = valid ? offer_trig(c, ws.lab[lane] - 1, xv, e) : false;
+    if (__any_sync(0xffffffffu, trig)) hmax_refresh_warp(c, lane);
+    const uint32_t nv = __popc(vm);
+    if (lane == 0) c.points += nv + (nv < q ? 1 : 0);
+    if (nv < q) return EL_DONE;
+    i += q;
+    if (i > m) return EL_DONE;
+    if constexpr (F == FAM_PMH2) x = __shfl_sync(0xffffffffu, xv, q - 1);
+    off = ws.next_off;
+    __syncwarp();
+  }
+}
+
+template <int F>
+__device__ __forceinline__ int warp_element(SetCtx& c, const Tables& T, WarpScratch& ws,
+                                            uint32_t* fy, int lane, int64_t e, uint64_t id,
+                                            double winv) {
+  if constexpr (F == FAM_PMH1 || F == FAM_PMH3 || F == FAM_UW3)
+    return warp_el_static<F>(c, T, ws, lane, e, id, winv);
+  else
+    return warp_el_fy<F>(c, T, ws, fy, lane, e, id, winv);
+}
+
+}  // namespace pmh
