@@ -19,6 +19,7 @@
 #include "../../include/pmh.h"
 #include "pmh_pminhash.cuh"
 #include "pmh_kernel.cuh"
+#include "pmh_order.cuh"
 
 using namespace pmh;
 
@@ -175,6 +176,95 @@ cudaError_t launch_pminhash(const PMinArgs& a, cudaStream_t st) {
   }
 }
 
+// Build the LPT set order on `st` into workspace: int32 order[nsets], 64 u32
+// bucket cursors, u32 counts[2] ([0] = number of sets with n > small_n, which
+// form the order prefix).  small_n < 0 disables the small-set split.
+struct OrderWs {
+  int32_t* order = nullptr;
+  unsigned* counts = nullptr;
+  void* mem = nullptr;
+};
+
+cudaError_t build_order(const int64_t* offsets, int64_t nsets, int64_t c, int64_t small_n,
+                        cudaStream_t st, OrderWs* ow) {
+  void* ws = nullptr;
+  const size_t hb = sizeof(unsigned) * (ORDER_BUCKETS + 2);
+  cudaError_t e = cudaMallocAsync(&ws, hb + sizeof(int32_t) * (size_t)nsets, st);
+  if (e != cudaSuccess) return e;
+  unsigned* hist = (unsigned*)ws;
+  unsigned* counts = hist + ORDER_BUCKETS;
+  int32_t* order = (int32_t*)((char*)ws + hb);
+  if ((e = cudaMemsetAsync(hist, 0, hb, st)) != cudaSuccess) return e;
+  int64_t blocks = (nsets + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  order_hist_kernel<<<(unsigned)blocks, 256, 0, st>>>(offsets, nsets, c, small_n, hist, counts);
+  order_scan_kernel<<<1, 32, 0, st>>>(hist);
+  order_scatter_kernel<<<(unsigned)blocks, 256, 0, st>>>(offsets, nsets, c, small_n, hist, order);
+  ow->order = order;
+  ow->counts = counts;
+  ow->mem = ws;
+  return cudaGetLastError();
+}
+
+// per-device auxiliary stream + events for the concurrent small-set kernel
+struct AuxStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+std::map<int, AuxStream> g_aux;
+
+int get_aux(AuxStream** out) {
+  int dev = 0;
+  PMH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_aux.find(dev);
+  if (it == g_aux.end()) {
+    AuxStream a;
+    PMH_CUDA(cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking));
+    PMH_CUDA(cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming));
+    PMH_CUDA(cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming));
+    it = g_aux.emplace(dev, a).first;
+  }
+  *out = &it->second;
+  return PMH_OK;
+}
+
+template <int F>
+cudaError_t launch_small(const SketchArgs& a, cudaStream_t st) {
+  const size_t per_warp = small_warp_bytes(F, a.m);
+  int wpc = (int)((96 * 1024) / per_warp);
+  wpc = wpc < 1 ? 1 : (wpc > 4 ? 4 : wpc);
+  const size_t smem = per_warp * (size_t)wpc;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(sketch_small_kernel<F>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int64_t grid = (a.nsets + wpc - 1) / wpc;
+  if (grid > 148 * 16) grid = 148 * 16;
+  sketch_small_kernel<F><<<(unsigned)grid, 32 * wpc, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// argument validation with the reference's error domain (sketch.py:96-114);
+// runs before any CUDA call
+int validate_sketch(int algo, int64_t m, const double* weights, int64_t nsets) {
+  const int fam = family_of(algo);
+  if (algo != ALG_PMINHASH && algo != ALG_MINHASH && fam == 0)
+    return set_error(PMH_ERR_INVALID, "unsupported algorithm id " + std::to_string(algo));
+  if (m < min_m(algo))
+    return set_error(PMH_ERR_INVALID, "signature size must be >= " + std::to_string(min_m(algo)));
+  if (algo != ALG_PMINHASH && algo != ALG_MINHASH &&
+      sketch_smem_bytes(fam, m, SKETCH_THREADS) > 227 * 1024)
+    return set_error(PMH_ERR_INVALID, "signature size too large for the shared-memory slot table");
+  if ((algo == ALG_PMINHASH || algo == ALG_MINHASH) && m > 64LL * PMIN_THREADS)
+    return set_error(PMH_ERR_INVALID, "signature size too large for the P-MinHash kernel");
+  if (m > 65535) return set_error(PMH_ERR_INVALID, "signature size must be <= 65535");
+  if (nsets < 0) return set_error(PMH_ERR_INVALID, "negative set count");
+  if (nsets > 0 && !is_unweighted(algo) && !weights)
+    return set_error(PMH_ERR_INVALID, "weighted algorithm requires weights");
+  return PMH_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -212,36 +302,35 @@ int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
                          int64_t* d_status, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int fam = family_of(algo);
-  if (algo != ALG_PMINHASH && algo != ALG_MINHASH && fam == 0)
-    return set_error(PMH_ERR_INVALID, "unsupported algorithm id " + std::to_string(algo));
-  if (m < min_m(algo))
-    return set_error(PMH_ERR_INVALID, "signature size must be >= " + std::to_string(min_m(algo)));
-  if (algo != ALG_PMINHASH && algo != ALG_MINHASH &&
-      sketch_smem_bytes(fam, m, SKETCH_THREADS) > 227 * 1024)
-    return set_error(PMH_ERR_INVALID, "signature size too large for the shared-memory slot table");
-  if (m > 65535) return set_error(PMH_ERR_INVALID, "signature size must be <= 65535");
-  if (nsets < 0) return set_error(PMH_ERR_INVALID, "negative set count");
+  int vrc = validate_sketch(algo, m, weights, nsets);
+  if (vrc != PMH_OK) return vrc;
   if (nsets == 0) return PMH_OK;
-  if (!is_unweighted(algo) && !weights)
-    return set_error(PMH_ERR_INVALID, "weighted algorithm requires weights");
   if (!d_status) return set_error(PMH_ERR_INVALID, "status buffer required");
   unsigned long long* flags = reinterpret_cast<unsigned long long*>(d_status);
   long long* d_err_set = reinterpret_cast<long long*>(d_status + 1);
 
   cudaError_t e;
-  if (algo == ALG_PMINHASH || algo == ALG_MINHASH) {
-    PMinArgs a{ids, algo == ALG_PMINHASH ? weights : nullptr, offsets, nullptr, nsets, m,
+  const bool pmin = algo == ALG_PMINHASH || algo == ALG_MINHASH;
+  OrderWs ow;
+  // cost offset: ProbMinHash families pay ~m ln m points per set regardless of n
+  e = build_order(offsets, nsets, pmin ? 0 : (int64_t)(7.0 * (double)m), pmin ? -1 : SMALL_N,
+                  st, &ow);
+  if (e != cudaSuccess) return cuda_fail(e, "set ordering");
+  int32_t* order = ow.order;
+  void* order_ws = ow.mem;
+  if (pmin) {
+    PMinArgs a{ids, algo == ALG_PMINHASH ? weights : nullptr, offsets, order, nsets, m,
                sig_out, stats_out, d_err_set};
     e = algo == ALG_PMINHASH ? launch_pminhash<true>(a, st) : launch_pminhash<false>(a, st);
   } else {
     const Tables* tp = nullptr;
     int rc = get_tables(fam, m, &tp);
-    if (rc) return rc;
+    if (rc) { cudaFreeAsync(order_ws, st); return rc; }
     SketchArgs a{};
     a.ids = ids;
     a.w = is_unweighted(algo) ? nullptr : weights;
     a.offsets = offsets;
-    a.order = nullptr;
+    a.order = order;
     a.nsets = nsets;
     a.m = m;
     a.sig = sig_out;
@@ -250,6 +339,14 @@ int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
     a.err_set = d_err_set;
     a.T = *tp;
     a.tconst = 4.0;
+    a.counts = ow.counts;
+    // small sets run warp-per-set on the auxiliary stream, concurrently with
+    // the CTA-per-set kernel on `st` (fork/join with events)
+    AuxStream* aux = nullptr;
+    rc = get_aux(&aux);
+    if (rc) { cudaFreeAsync(order_ws, st); return rc; }
+    PMH_CUDA(cudaEventRecord(aux->fork, st));
+    PMH_CUDA(cudaStreamWaitEvent(aux->s, aux->fork, 0));
     switch (fam) {
       case FAM_PMH1: e = launch_family<FAM_PMH1>(a, st); break;
       case FAM_PMH2: e = launch_family<FAM_PMH2>(a, st); break;
@@ -258,7 +355,20 @@ int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
       case FAM_UW3: e = launch_family<FAM_UW3>(a, st); break;
       default: e = launch_family<FAM_UW4>(a, st); break;
     }
+    if (e == cudaSuccess) {
+      switch (fam) {
+        case FAM_PMH1: e = launch_small<FAM_PMH1>(a, aux->s); break;
+        case FAM_PMH2: e = launch_small<FAM_PMH2>(a, aux->s); break;
+        case FAM_PMH3: e = launch_small<FAM_PMH3>(a, aux->s); break;
+        case FAM_PMH4: e = launch_small<FAM_PMH4>(a, aux->s); break;
+        case FAM_UW3: e = launch_small<FAM_UW3>(a, aux->s); break;
+        default: e = launch_small<FAM_UW4>(a, aux->s); break;
+      }
+    }
+    cudaEventRecord(aux->join, aux->s);
+    cudaStreamWaitEvent(st, aux->join, 0);
   }
+  cudaFreeAsync(order_ws, st);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   if (stats_out && !reports_buffer(algo) && algo != ALG_PMINHASH && algo != ALG_MINHASH) {
     // the non-interleaved variants have no buffer (K:334-336): column 1 = 0
@@ -274,7 +384,9 @@ int pmh_sketch_csr(int algo, int64_t m, const uint64_t* ids,
                    int64_t* err_set, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (err_set) *err_set = -1;
-  if (nsets == 0 && m >= min_m(algo)) return PMH_OK;
+  int vrc = validate_sketch(algo, m, weights, nsets);
+  if (vrc != PMH_OK) return vrc;
+  if (nsets == 0) return PMH_OK;
   int64_t* d_status = nullptr;
   PMH_CUDA(cudaMallocAsync((void**)&d_status, 16, st));
   int rc = pmh_status_reset(d_status, st);

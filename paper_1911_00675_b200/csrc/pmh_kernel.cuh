@@ -51,7 +51,10 @@ __global__ void __launch_bounds__(SKETCH_THREADS) sketch_sets_kernel(SketchArgs 
   // parses its bit offsets (Fisher-Yates families)
   const bool warp_ok = family_uses_fy(F) || ((m & (m - 1)) == 0);
 
-  for (int64_t bs = blockIdx.x; bs < a.nsets; bs += gridDim.x) {
+  // with a small-set kernel running beside it, this kernel takes the large
+  // sets only: the prefix order[0, counts[0]) of the LPT order
+  const int64_t n_mine = a.counts ? (int64_t)a.counts[0] : a.nsets;
+  for (int64_t bs = blockIdx.x; bs < n_mine; bs += gridDim.x) {
     const int64_t s = a.order ? (int64_t)a.order[bs] : bs;
     const int64_t off = a.offsets[s];
     const int64_t n = a.offsets[s + 1] - off;
@@ -171,6 +174,139 @@ __global__ void __launch_bounds__(SKETCH_THREADS) sketch_sets_kernel(SketchArgs 
       }
     }
     __syncthreads();
+  }
+}
+
+}  // namespace pmh
+
+namespace pmh {
+
+// ---------------------------------------------------------------------------
+// Small sets (n <= SMALL_N): one WARP per set.  Their cost is the coupon-
+// collector phase (~m (ln m + c) points, all in long per-element sequences),
+// so every element runs warp-cooperatively (mode B) and a CTA-per-set layout
+// would idle 7 of 8 warps.  Each warp owns a private slot table, scratch and
+// Fisher-Yates map in shared memory.
+// ---------------------------------------------------------------------------
+constexpr int64_t SMALL_N = 3;   // measured: warp-per-set wins only below ~4 elements
+
+struct WarpSetVars {
+  unsigned long long hmax;
+  unsigned int filled;
+  unsigned int pad;
+};
+
+__host__ __device__ inline size_t small_warp_bytes(int family, int64_t m) {
+  size_t b = sizeof(Slot) * (size_t)m + sizeof(WarpScratch) + sizeof(WarpSetVars);
+  if (family_uses_fy(family)) b += sizeof(uint32_t) * (size_t)(m + 1);
+  return (b + 15) & ~(size_t)15;
+}
+
+template <int F>
+__global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wpc = blockDim.x >> 5;
+  const int64_t m = a.m;
+  unsigned char* base = smem + small_warp_bytes(F, m) * (size_t)wid;
+  Slot* slots = reinterpret_cast<Slot*>(base);
+  WarpScratch* ws = reinterpret_cast<WarpScratch*>(base + sizeof(Slot) * m);
+  WarpSetVars* wv = reinterpret_cast<WarpSetVars*>(base + sizeof(Slot) * m + sizeof(WarpScratch));
+  uint32_t* fy = reinterpret_cast<uint32_t*>(base + sizeof(Slot) * m + sizeof(WarpScratch) +
+                                             sizeof(WarpSetVars));
+  if (family_uses_fy(F)) {
+    for (int64_t p = lane; p <= m; p += 32) fy[p] = 0;
+    if (lane == 0) ws->epoch = 0;
+  }
+  const int64_t n_large = (int64_t)a.counts[0];
+  const int64_t n_small = a.nsets - n_large;
+  const bool warp_ok = family_uses_fy(F) || ((m & (m - 1)) == 0);
+  for (int64_t bs = (int64_t)blockIdx.x * wpc + wid; bs < n_small; bs += (int64_t)gridDim.x * wpc) {
+    const int64_t s = (int64_t)a.order[n_large + bs];
+    const int64_t off = a.offsets[s];
+    const int64_t n = a.offsets[s + 1] - off;
+    if (n <= 0) {
+      if (lane == 0) atomicMin(a.err_set, (long long)s);
+      continue;
+    }
+    const uint64_t* ids = a.ids + off;
+    const double* w = a.w ? a.w + off : nullptr;
+    for (int64_t k = lane; k < m; k += 32) { slots[k].h = EMPTY_H; slots[k].idx = EMPTY_IDX; }
+    double W = 0.0;
+    if (family_weighted(F) && w) {
+      for (int64_t e = lane; e < n; e += 32) W += w[e];
+      for (int o = 16; o > 0; o >>= 1) W += __shfl_xor_sync(0xffffffffu, W, o);
+    } else {
+      W = (double)n;
+    }
+    if (lane == 0) { wv->hmax = EMPTY_H; wv->filled = 0; }
+    __syncwarp();
+    SetCtx c;
+    c.slots = slots;
+    c.hmax_bits = &wv->hmax;
+    c.filled = &wv->filled;
+    c.m = m;
+    c.kbits = bits_for(m);
+    c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
+    c.points = 0; c.updates = 0; c.multi = 0;
+    double tg = (double)m * (log((double)m) + a.tconst) / W;
+    if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
+    bool failed = false;
+    for (int attempt = 0;; attempt++) {
+      c.tguess = tg;
+      for (int64_t e = 0; e < n && !failed; e++) {
+        const uint64_t id = ids[e];
+        const double winv = (family_weighted(F) && w) ? 1.0 / w[e] : 1.0;
+        int st;
+        if (warp_ok) {
+          st = warp_element<F>(c, a.T, *ws, fy, lane, e, id, winv);
+        } else {
+          st = EL_DONE;
+          if (lane == 0) {
+            SparseFY sfy; sfy.reset();
+            st = run_element<F>(c, a.T, sfy, e, id, winv);
+            if (st == EL_DONE) hmax_recompute_serial(c);
+          }
+          st = __shfl_sync(0xffffffffu, st, 0);
+        }
+        if (st == EL_FAIL) failed = true;
+        if (lane == 0) c.multi++;
+        __syncwarp();
+      }
+      unsigned long long mx = 0;
+      for (int64_t k = lane; k < m; k += 32) {
+        const unsigned long long h = slots[k].h;
+        mx = h > mx ? h : mx;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = v > mx ? v : mx;
+      }
+      if (failed || !(__longlong_as_double((long long)mx) > tg)) break;
+      tg = attempt >= 2 ? __longlong_as_double(0x7FF0000000000000LL) : tg * 4.0;
+    }
+    if (failed && lane == 0) {
+      atomicOr(a.err_flags, (unsigned long long)ERRF_RANDOMNESS);
+      atomicMin(a.err_set, (long long)s);
+    }
+    uint64_t* sig = a.sig + (size_t)s * m;
+    for (int64_t k = lane; k < m; k += 32) {
+      const unsigned long long ix = slots[k].idx;
+      sig[k] = ix < (unsigned long long)n ? ids[ix] : 0ULL;
+    }
+    if (a.stats) {
+      long long pts = c.points, upd = c.updates;
+      for (int o = 16; o > 0; o >>= 1) {
+        pts += __shfl_xor_sync(0xffffffffu, pts, o);
+        upd += __shfl_xor_sync(0xffffffffu, upd, o);
+      }
+      if (lane == 0) {
+        a.stats[s * 3 + 0] = pts;
+        a.stats[s * 3 + 1] = c.multi;
+        a.stats[s * 3 + 2] = upd;
+      }
+    }
+    __syncwarp();
   }
 }
 

@@ -345,6 +345,7 @@ struct SketchArgs {
   long long* err_set;       // device, min failing set index
   Tables T;
   double tconst;            // threshold-guess constant (ln m + tconst)
+  const unsigned* counts;   // device: [0] = number of large sets (order prefix)
 };
 
 __device__ __forceinline__ double block_sum(double v, double* red) {

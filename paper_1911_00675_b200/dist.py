@@ -1,0 +1,169 @@
+"""Multi-GPU driver (one process per GPU, torch.distributed).
+
+Sketching shards: sets are independent, so each rank sketches a contiguous
+range of sets chosen to balance ESTIMATED COST (not element count): a
+ProbMinHash set costs about n + m (ln m + 4) points (the coupon-collector
+phase dominates small sets), a P-MinHash set n * m draws.  No collective is
+needed on the sketch path.
+
+All-pairs estimation (configs[4]) has one real exchange step: an all-gather
+of the [N, m] signature matrix (NCCL over NVLink/NVSwitch on the GPU box),
+then each rank computes a balanced share of upper-triangle block rows with
+the tiled equal-component kernel and a histogram/threshold reduction; the
+per-rank histograms are summed with one all_reduce.
+
+Every compute step is a callable so the orchestration is testable on CPU
+(gloo, world_size 2) with the oracle injected in tests; the defaults call
+libpmh.so on the rank's GPU.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def set_costs(offsets, m: int, algo: str) -> np.ndarray:
+    sizes = np.diff(np.asarray(offsets, np.int64)).astype(np.float64)
+    if algo in ("pminhash", "minhash"):
+        return sizes * m
+    return sizes + m * (math.log(m) + 4.0)
+
+
+def shard_ranges(offsets, world: int, m: int = 1024, algo: str = "probminhash3"):
+    """Contiguous set ranges [(s0, s1)] per rank with near-equal total cost
+    (greedy split of the cumulative cost curve)."""
+    costs = set_costs(offsets, m, algo)
+    S = costs.size
+    if world <= 1 or S == 0:
+        return [(0, S)]
+    cum = np.concatenate([[0.0], np.cumsum(costs)])
+    total = cum[-1]
+    bounds = [0]
+    for r in range(1, world):
+        target = total * r / world
+        b = int(np.searchsorted(cum, target, side="left"))
+        b = min(max(b, bounds[-1]), S)
+        bounds.append(b)
+    bounds.append(S)
+    return [(bounds[r], bounds[r + 1]) for r in range(world)]
+
+
+def local_batch(batch, rng):
+    """Slice a CSRBatch to sets [s0, s1) with rebased offsets."""
+    s0, s1 = rng
+    a, b = int(batch.offsets[s0]), int(batch.offsets[s1])
+    from .datagen import CSRBatch
+    w = None if batch.weights is None else batch.weights[a:b]
+    return CSRBatch(batch.ids[a:b], w, batch.offsets[s0:s1 + 1] - a, batch.name + f"[{s0}:{s1}]")
+
+
+def _gpu_sketch(algo, m, batch):
+    import torch
+    from . import sketch_batch
+    from .batch import to_device_f64, to_device_i64, to_device_u64
+    ids = to_device_u64(batch.ids)
+    w = to_device_f64(batch.weights) if batch.weights is not None else None
+    off = to_device_i64(batch.offsets)
+    sig, _ = sketch_batch(algo, ids, w, off, m, want_stats=False)
+    torch.cuda.synchronize()
+    return sig
+
+
+def sketch_sharded(algo, m, batch, rank, world, sketch_fn=None):
+    """Each rank sketches its cost-balanced range; returns (range, local sigs).
+    No collective: signatures stay sharded."""
+    rng = shard_ranges(batch.offsets, world, m, algo)[rank]
+    fn = sketch_fn or _gpu_sketch
+    return rng, fn(algo, m, local_batch(batch, rng))
+
+
+# ---------------------------------------------------------------------------
+# all-pairs
+# ---------------------------------------------------------------------------
+
+def block_rows(n: int, tile: int, world: int):
+    """Balanced assignment of upper-triangle block rows to ranks: block row b
+    has (nb - b) tiles; rows are dealt in a serpentine order so every rank
+    gets a near-equal tile count."""
+    nb = (n + tile - 1) // tile
+    order = sorted(range(nb), key=lambda b: -(nb - b))
+    loads = [0] * world
+    assign = [[] for _ in range(world)]
+    for b in order:
+        r = min(range(world), key=lambda q: loads[q])
+        assign[r].append(b)
+        loads[r] += nb - b
+    return [sorted(a) for a in assign]
+
+
+@dataclass
+class AllPairsResult:
+    hist: np.ndarray          # int64[m+1]: number of pairs (i<j) with count c
+    pairs: np.ndarray         # int64[K, 3]: (i, j, count) with count >= threshold
+    tiles: int
+
+
+def allpairs_local(sigs_all, rows, tile, threshold, count_tile_fn):
+    """Compute this rank's block rows: histogram + pairs above threshold.
+
+    count_tile_fn(sigs_all, r0, r1, c0, c1) -> int array (r1-r0, c1-c0) of
+    equal-component counts (only j > i entries are used)."""
+    n, m = sigs_all.shape
+    hist = np.zeros(m + 1, np.int64)
+    found = []
+    tiles = 0
+    for b in rows:
+        r0, r1 = b * tile, min(n, (b + 1) * tile)
+        for c0 in range(r0, n, tile):
+            c1 = min(n, c0 + tile)
+            cnt = np.asarray(count_tile_fn(sigs_all, r0, r1, c0, c1))
+            ii = np.arange(r0, r1)[:, None]
+            jj = np.arange(c0, c1)[None, :]
+            upper = jj > ii
+            vals = cnt[upper].astype(np.int64)
+            hist += np.bincount(vals, minlength=m + 1)[: m + 1]
+            sel = upper & (cnt >= threshold)
+            if sel.any():
+                iw, jw = np.nonzero(sel)
+                found.append(np.stack([iw + r0, jw + c0, cnt[sel]], axis=1).astype(np.int64))
+            tiles += 1
+    pairs = np.concatenate(found) if found else np.zeros((0, 3), np.int64)
+    return AllPairsResult(hist, pairs, tiles)
+
+
+def _gpu_count_tile(sigs_all, r0, r1, c0, c1):
+    from .batch import allpairs_tile_device
+    out = allpairs_tile_device(sigs_all, r0, r1, c0, c1)
+    return out.cpu().numpy().view(np.uint16)
+
+
+def allpairs_distributed(local_sigs, rank, world, tile=4096, threshold=1, group=None,
+                         count_tile_fn=None):
+    """All-gather the sharded signatures, compute this rank's block rows and
+    all_reduce the histogram.  local_sigs: torch tensor [n_r, m] (int64, on
+    the rank's device for NCCL; CPU for gloo).  Ranks may hold different row
+    counts (padded for the all_gather)."""
+    import torch
+    import torch.distributed as dist
+    n_r = torch.tensor([local_sigs.shape[0]], device=local_sigs.device, dtype=torch.int64)
+    sizes = [torch.zeros_like(n_r) for _ in range(world)]
+    dist.all_gather(sizes, n_r, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    mx = max(sizes)
+    m = local_sigs.shape[1]
+    pad = torch.zeros((mx, m), dtype=local_sigs.dtype, device=local_sigs.device)
+    pad[: local_sigs.shape[0]] = local_sigs
+    gathered = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(gathered, pad, group=group)
+    sigs_all = torch.cat([g[:s] for g, s in zip(gathered, sizes)], dim=0)
+    n = sigs_all.shape[0]
+    rows = block_rows(n, tile, world)[rank]
+    fn = count_tile_fn or _gpu_count_tile
+    res = allpairs_local(sigs_all, rows, tile, threshold, fn)
+    h = torch.from_numpy(res.hist).to(local_sigs.device)
+    dist.all_reduce(h, group=group)
+    res.hist = h.cpu().numpy()
+    return res

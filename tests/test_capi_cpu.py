@@ -1,0 +1,107 @@
+"""CPU-side checks of the C ABI library: it loads without a GPU, exports every
+symbol include/pmh.h declares, validates arguments with the reference's error
+domain, and the host-side package mirrors the reference API surface."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1911_00675_b200 import _lib
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def _header_symbols():
+    src = open(os.path.join(ROOT, "include", "pmh.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(pmh_\w+)\s*\(", src, re.M)))
+
+
+def test_library_loads_and_exports_header_symbols():
+    L = _lib.load()
+    syms = _header_symbols()
+    assert len(syms) >= 10
+    for name in syms:
+        assert hasattr(L, name), name
+    assert set(syms) == set(_lib.EXPORTS)
+    assert L.pmh_version() >= 100
+
+
+def test_invalid_params_rejected_without_gpu():
+    """Host-side validation happens before any CUDA call (sketch.py:96-114)."""
+    L = _lib.load()
+    err = ctypes.c_int64(0)
+    # PMH3 needs m >= 2
+    rc = L.pmh_sketch_csr(_lib.ALG["probminhash3"], 1, None, None, None, 1, None, None,
+                          ctypes.byref(err), None)
+    assert rc == _lib.PMH_ERR_INVALID
+    # unknown algorithm
+    rc = L.pmh_sketch_csr(99, 16, None, None, None, 1, None, None, ctypes.byref(err), None)
+    assert rc == _lib.PMH_ERR_INVALID
+    # b out of range
+    assert L.pmh_bbit(None, 1, 16, 0, None, None) == _lib.PMH_ERR_INVALID
+    assert L.pmh_bbit(None, 1, 16, 17, None, None) == _lib.PMH_ERR_INVALID
+    # empty batch is a no-op
+    assert L.pmh_sketch_csr(_lib.ALG["probminhash1"], 16, None, None, None, 0, None, None,
+                            ctypes.byref(err), None) == _lib.PMH_OK
+
+
+def test_error_mapping_to_reference_exceptions():
+    from paper_1911_00675_b200 import (EmptyInputError, InvalidParamsError,
+                                       RandomnessFailureError)
+    with pytest.raises(InvalidParamsError):
+        _lib.check(_lib.PMH_ERR_INVALID)
+    with pytest.raises(EmptyInputError):
+        _lib.check(_lib.PMH_ERR_EMPTY)
+    with pytest.raises(RandomnessFailureError):
+        _lib.check(_lib.PMH_ERR_RANDOMNESS)
+    assert issubclass(EmptyInputError, ValueError)
+    assert issubclass(RandomnessFailureError, RuntimeError)
+
+
+def test_public_names_match_reference_surface():
+    import paper_1911_00675_b200 as pkg
+    # the reference's __all__ (/root/reference/pkg/src/probminhash/__init__.py:50-89)
+    ref_all = {
+        "BBitSignature", "EmptyInputError", "InvalidParamsError", "LazyPermutation",
+        "RandomStream", "RandomnessFailureError", "Signature", "SketchParams", "SketchStats",
+        "StopLimitTree", "TruncExpParams", "WEIGHTED_ALGORITHMS", "WeightPairMultiset",
+        "WeightedSet", "bbit_reduce", "estimate_similarity", "estimate_similarity_bbit",
+        "estimator_variance", "improvement_factor", "jaccard_exact", "jaccard_n_exact",
+        "jaccard_p_exact", "jaccard_w_exact", "minhash", "new_stream", "oph_densified",
+        "perm_new", "pminhash", "probminhash1", "probminhash1a", "probminhash2",
+        "probminhash3", "probminhash3a", "probminhash4", "sketch_unweighted", "superminhash",
+        "superminhash_variance", "tree_new"}
+    assert ref_all <= set(pkg.__all__)
+    for n in ref_all:
+        assert hasattr(pkg, n), n
+
+
+def test_host_validation_mirrors_reference():
+    from paper_1911_00675_b200 import InvalidParamsError, SketchParams, WeightedSet
+    import math
+    with pytest.raises(InvalidParamsError):
+        WeightedSet([(1, 0.0)])
+    with pytest.raises(InvalidParamsError):
+        WeightedSet([(1, -2.0)])
+    with pytest.raises(InvalidParamsError):
+        WeightedSet([(1, math.inf)])
+    with pytest.raises(InvalidParamsError):
+        WeightedSet([(1, 1.0), (1, 2.0)])
+    with pytest.raises(InvalidParamsError):
+        WeightedSet.from_arrays([1, 2], [1.0])
+    with pytest.raises(InvalidParamsError):
+        SketchParams(0)
+    ws = WeightedSet([(5, 1.5), (7, 2.0)])
+    assert len(ws) == 2 and ws.ids.dtype == np.uint64
+
+
+def test_compute_fails_loudly_without_cuda(monkeypatch):
+    """No CPU fallback: without a CUDA device the product path raises."""
+    import torch
+    from paper_1911_00675_b200 import WeightedSet, probminhash1
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError):
+        probminhash1(WeightedSet([(1, 1.0)]), 8)

@@ -1,0 +1,101 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the multi-GPU driver's
+host logic: cost-balanced sharding, sharded sketch reassembly, and the
+all-gather + block-row all-pairs with an all_reduce'd histogram.  The GPU
+compute steps are replaced by the CPU oracle (test infrastructure)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as orc
+from paper_1911_00675_b200 import datagen
+from paper_1911_00675_b200 import dist as pdist
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_sketch(algo, m, b):
+    sig, _ = orc.sketch_csr(algo, m, b.ids, b.weights, b.offsets)
+    return torch.from_numpy(sig.view(np.int64))
+
+
+def _oracle_tile(sigs_all, r0, r1, c0, c1):
+    s = sigs_all.numpy().view(np.uint64)
+    a = s[r0:r1][:, None, :]
+    b = s[c0:c1][None, :, :]
+    return (a == b).sum(axis=2)
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        batch = datagen.random_sets(3, [5, 40, 1, 300, 17, 2, 90, 12, 7, 33], "exp")
+        m = 32
+        rng, sig = pdist.sketch_sharded("probminhash4", m, batch, rank, world,
+                                        sketch_fn=_oracle_sketch)
+        res = pdist.allpairs_distributed(sig, rank, world, tile=3, threshold=1,
+                                         count_tile_fn=_oracle_tile)
+        q.put((rank, rng, sig.numpy().copy(), res.hist.copy(), res.pairs.copy(), res.tiles))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_ranges_balanced_and_complete():
+    b = datagen.config2(nsets=2000)
+    for world in (1, 2, 4, 8):
+        rngs = pdist.shard_ranges(b.offsets, world, 1024, "probminhash3")
+        assert rngs[0][0] == 0 and rngs[-1][1] == b.nsets
+        assert all(rngs[i][1] == rngs[i + 1][0] for i in range(world - 1))
+        c = pdist.set_costs(b.offsets, 1024, "probminhash3")
+        loads = [c[a:z].sum() for a, z in rngs]
+        assert max(loads) <= 1.15 * c.sum() / world + c.max()
+
+
+def test_block_rows_cover_triangle_balanced():
+    for n, tile, world in ((1000, 64, 3), (100000, 4096, 8), (10, 3, 2)):
+        rows = pdist.block_rows(n, tile, world)
+        nb = (n + tile - 1) // tile
+        assert sorted(sum(rows, [])) == list(range(nb))
+        loads = [sum(nb - b for b in r) for r in rows]
+        assert max(loads) - min(loads) <= nb
+
+
+def test_gloo_world2_sharded_sketch_and_allpairs():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    batch = datagen.random_sets(3, [5, 40, 1, 300, 17, 2, 90, 12, 7, 33], "exp")
+    m = 32
+    ref, _ = orc.sketch_csr("probminhash4", m, batch.ids, batch.weights, batch.offsets)
+    got = np.concatenate([o[2] for o in out]).view(np.uint64)
+    np.testing.assert_array_equal(got, ref)
+    # all-pairs: reduced histogram and union of pairs match a single-process pass
+    full = orc.allpairs(ref)
+    n = ref.shape[0]
+    iu = np.triu_indices(n, 1)
+    exp_hist = np.bincount(full[iu], minlength=m + 1)
+    np.testing.assert_array_equal(out[0][3], exp_hist)
+    np.testing.assert_array_equal(out[1][3], exp_hist)
+    pairs = np.concatenate([o[4] for o in out])
+    exp_pairs = {(int(i), int(j), int(full[i, j])) for i, j in zip(*iu) if full[i, j] >= 1}
+    assert {tuple(map(int, p)) for p in pairs} == exp_pairs

@@ -13,9 +13,11 @@ v = sys.argv[1]
 minn = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 M = int(sys.argv[4]) if len(sys.argv) > 4 else 1024
+maxn = int(sys.argv[5]) if len(sys.argv) > 5 else 0
 full = datagen.config2()
 sizes = np.diff(full.offsets)
-b = full.subset(np.nonzero(sizes >= minn)[0]) if minn else full
+sel = (sizes >= minn) & ((sizes <= maxn) if maxn else True)
+b = full.subset(np.nonzero(sel)[0]) if (minn or maxn) else full
 ids, w, off = to_device_u64(b.ids), to_device_f64(b.weights), to_device_i64(b.offsets)
 sig = torch.empty((b.nsets, M), dtype=torch.int64, device="cuda")
 L = _lib.load()
