@@ -9,6 +9,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -181,27 +182,31 @@ cudaError_t launch_pminhash(const PMinArgs& a, cudaStream_t st) {
 // form the order prefix).  small_n < 0 disables the small-set split.
 struct OrderWs {
   int32_t* order = nullptr;
-  unsigned* counts = nullptr;
+  unsigned* counts = nullptr;          // [0] #sets n > small_n, [1] #sets n >= big_n
+  unsigned long long* ctr = nullptr;   // two work counters
   void* mem = nullptr;
 };
 
 cudaError_t build_order(const int64_t* offsets, int64_t nsets, int64_t c, int64_t small_n,
-                        cudaStream_t st, OrderWs* ow) {
+                        int64_t big_n, cudaStream_t st, OrderWs* ow) {
   void* ws = nullptr;
-  const size_t hb = sizeof(unsigned) * (ORDER_BUCKETS + 2);
+  const size_t hb = sizeof(unsigned) * (ORDER_BUCKETS + 4) + sizeof(unsigned long long) * 2;
   cudaError_t e = cudaMallocAsync(&ws, hb + sizeof(int32_t) * (size_t)nsets, st);
   if (e != cudaSuccess) return e;
   unsigned* hist = (unsigned*)ws;
   unsigned* counts = hist + ORDER_BUCKETS;
+  unsigned long long* ctr = (unsigned long long*)(hist + ORDER_BUCKETS + 4);
   int32_t* order = (int32_t*)((char*)ws + hb);
   if ((e = cudaMemsetAsync(hist, 0, hb, st)) != cudaSuccess) return e;
   int64_t blocks = (nsets + 255) / 256;
   if (blocks > 1184) blocks = 1184;
-  order_hist_kernel<<<(unsigned)blocks, 256, 0, st>>>(offsets, nsets, c, small_n, hist, counts);
+  order_hist_kernel<<<(unsigned)blocks, 256, 0, st>>>(offsets, nsets, c, small_n, big_n, hist,
+                                                      counts);
   order_scan_kernel<<<1, 32, 0, st>>>(hist);
   order_scatter_kernel<<<(unsigned)blocks, 256, 0, st>>>(offsets, nsets, c, small_n, hist, order);
   ow->order = order;
   ow->counts = counts;
+  ow->ctr = ctr;
   ow->mem = ws;
   return cudaGetLastError();
 }
@@ -314,7 +319,7 @@ int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
   OrderWs ow;
   // cost offset: ProbMinHash families pay ~m ln m points per set regardless of n
   e = build_order(offsets, nsets, pmin ? 0 : (int64_t)(7.0 * (double)m), pmin ? -1 : SMALL_N,
-                  st, &ow);
+                  4096, st, &ow);
   if (e != cudaSuccess) return cuda_fail(e, "set ordering");
   int32_t* order = ow.order;
   void* order_ws = ow.mem;

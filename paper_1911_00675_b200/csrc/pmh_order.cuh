@@ -22,20 +22,27 @@ __device__ __forceinline__ int order_key(int64_t n, int64_t c, int64_t small_n) 
   return k > ORDER_BUCKETS - 1 ? ORDER_BUCKETS - 1 : k;
 }
 
+// counts[0] = #sets with n > small_n, counts[1] = #sets with n >= big_n
 __global__ void order_hist_kernel(const int64_t* __restrict__ offsets, int64_t nsets, int64_t c,
-                                  int64_t small_n, unsigned int* __restrict__ hist,
+                                  int64_t small_n, int64_t big_n, unsigned int* __restrict__ hist,
                                   unsigned int* __restrict__ n_large) {
   __shared__ unsigned int sh[ORDER_BUCKETS];
+  __shared__ unsigned int s_big;
   for (int i = threadIdx.x; i < ORDER_BUCKETS; i += blockDim.x) sh[i] = 0;
+  if (threadIdx.x == 0) s_big = 0;
   __syncthreads();
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nsets;
-       s += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&sh[order_key(offsets[s + 1] - offsets[s], c, small_n)], 1u);
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = offsets[s + 1] - offsets[s];
+    atomicAdd(&sh[order_key(n, c, small_n)], 1u);
+    if (n >= big_n) atomicAdd(&s_big, 1u);
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < ORDER_BUCKETS; i += blockDim.x) {
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
     if (i > 0 && sh[i]) atomicAdd(n_large, sh[i]);
   }
+  if (threadIdx.x == 0 && s_big) atomicAdd(n_large + 1, s_big);
 }
 
 // single warp: exclusive scan in DESCENDING key order -> bucket cursors

@@ -178,11 +178,22 @@ __global__ void __launch_bounds__(PMIN_THREADS) pminhash_kernel(PMinArgs a) {
 // groups prune with everyone's minima.
 // ---------------------------------------------------------------------------
 constexpr int PM64_C = 64;
+constexpr int PM64_REFRESH = 16;   // elements between threshold refreshes
+
+// Shared table layout: component k = 64 t + q (thread t, draw q) lives at
+// TRANSPOSED index q * tpg + t, so the 16..32 threads of a warp touch
+// consecutive 16-byte entries when they walk their own 64 components
+// (conflict-free refresh).
+__device__ __forceinline__ int64_t pm64_slot(int64_t t, int q, int tpg) {
+  return (int64_t)q * tpg + t;
+}
 
 // exact path for the flagged draws of one element (rare)
 template <bool EXPO>
-__device__ __noinline__ void pm64_candidates(uint64_t cand, uint64_t id, double winv, uint32_t e,
-                                             int64_t k0, Slot* table) {
+__device__ __noinline__ void pm64_candidates(uint64_t cand, uint64_t id, double w, uint32_t e,
+                                             int64_t t, int tpg, Slot* table) {
+  const double winv = EXPO ? 1.0 / w : 1.0;
+  const int64_t k0 = t * PM64_C;
   while (cand) {
     const int q = __ffsll((long long)cand) - 1;
     cand &= cand - 1;
@@ -193,7 +204,7 @@ __device__ __noinline__ void pm64_candidates(uint64_t cand, uint64_t id, double 
     uint64_t b = lo >> sh;
     if (sh > 11) b |= stream_word(id, wi + 2) << (64 - sh);
     b &= (1ULL << 53) - 1ULL;
-    Slot* sl = &table[k0 + q];
+    Slot* sl = &table[pm64_slot(t, q, tpg)];
     const double cur = __longlong_as_double((long long)*(volatile unsigned long long*)&sl->h);
     double h;
     if constexpr (EXPO) {
@@ -206,28 +217,28 @@ __device__ __noinline__ void pm64_candidates(uint64_t cand, uint64_t id, double 
   }
 }
 
-__device__ __forceinline__ double pm64_tmax(const Slot* table, int64_t k0) {
+__device__ __forceinline__ double pm64_tmax(const Slot* table, int64_t t, int tpg) {
   unsigned long long mx = 0;
 #pragma unroll 8
   for (int q = 0; q < PM64_C; q++) {
-    const unsigned long long h = *(volatile const unsigned long long*)&table[k0 + q].h;
+    const unsigned long long h =
+        *(volatile const unsigned long long*)&table[pm64_slot(t, q, tpg)].h;
     mx = h > mx ? h : mx;
   }
   return __longlong_as_double((long long)mx);
 }
 
+// Each group of tpg = m/64 threads walks its elements g, g + G, ... straight
+// from global memory (broadcast loads, next element prefetched): no block
+// barrier inside a set, so warps with more candidates do not stall the CTA.
 template <bool EXPO>
 __global__ void __launch_bounds__(PMIN_THREADS) pminhash64_kernel(PMinArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ uint64_t s_id[PMIN_CHUNK];
-  __shared__ double s_winv[PMIN_CHUNK];
-  __shared__ double s_sw[PMIN_CHUNK];
   const int64_t m = a.m;
   const int tpg = (int)(m / PM64_C);               // threads per group
   const int groups = PMIN_THREADS / tpg;
   const int g = threadIdx.x / tpg, t = threadIdx.x % tpg;
   const bool active = g < groups;
-  const int64_t k0 = (int64_t)t * PM64_C;
   Slot* table = reinterpret_cast<Slot*>(smem);
   const double two53m = 9007199254740992.0 * 1.0000000000009095;  // 2^53 (1 + 2^-40)
   const uint64_t wbase = 53ULL * (uint64_t)t + 1ULL;                // first word (1-based)
@@ -244,48 +255,54 @@ __global__ void __launch_bounds__(PMIN_THREADS) pminhash64_kernel(PMinArgs a) {
       table[k].h = EMPTY_H;
       table[k].idx = EMPTY_IDX;
     }
-    double tmax = __longlong_as_double(0x7FF0000000000000LL);
-    int since = 0;
-    for (int64_t c0 = 0; c0 < n; c0 += PMIN_CHUNK) {
-      const int64_t cn = n - c0 < PMIN_CHUNK ? n - c0 : PMIN_CHUNK;
-      __syncthreads();
-      if (threadIdx.x < cn) {
-        s_id[threadIdx.x] = a.ids[off + c0 + threadIdx.x];
-        if (EXPO) {
-          const double w = a.w ? a.w[off + c0 + threadIdx.x] : 1.0;
-          s_winv[threadIdx.x] = 1.0 / w;
-          s_sw[threadIdx.x] = w * two53m;
-        } else {
-          s_winv[threadIdx.x] = 1.0;
-          s_sw[threadIdx.x] = two53m;
+    __syncthreads();
+    if (active) {
+      const uint64_t* ids = a.ids + off;
+      const double* ws = (EXPO && a.w) ? a.w + off : nullptr;
+      double tmax = __longlong_as_double(0x7FF0000000000000LL);
+      int since = 0;
+      // groups per warp (2 when m = 1024): the trip count is made warp-uniform
+      // so a full-warp __syncwarp can reconverge the lanes every element
+      const int gpw = tpg >= 32 ? 1 : 32 / tpg;
+      const int gsub = g % gpw;
+      int64_t ew = g - gsub;                       // first group of this warp
+      int64_t e = ew + gsub;
+      uint64_t id_n = e < n ? __ldg(&ids[e]) : 0;
+      double w_n = (ws && e < n) ? __ldg(&ws[e]) : 1.0;
+      for (; ew < n; ew += groups) {
+        e = ew + gsub;
+        const bool live = e < n;
+        const uint64_t id = id_n;
+        const double w = w_n;
+        if (e + groups < n) {                      // prefetch the next element
+          id_n = __ldg(&ids[e + groups]);
+          if (ws) w_n = __ldg(&ws[e + groups]);
         }
-      }
-      __syncthreads();
-      if (!active) continue;
-      for (int64_t le = g; le < cn; le += groups) {
-        const uint64_t id = s_id[le];
-        const double tb = tmax * s_sw[le];
-        // b < Tb  =>  b >> 21 <= (Tb - 1) >> 21 ; Tb = floor(tb) + 1
+        const double tb = tmax * (w * two53m);
+        // b < Tb = floor(tb) + 1  =>  b >> 21 <= tb >> 21
         const uint32_t tbh = tb < 9007199254740992.0 ? (uint32_t)((uint64_t)tb >> 21)
                                                       : 0xFFFFFFFFu;
         uint64_t st = id + wbase * GOLDEN;
         uint32_t c_lo = 0, c_hi = 0;
 #include "pm64_body.inc"
-        const uint64_t cand = ((uint64_t)c_hi << 32) | c_lo;
+        const uint64_t cand = live ? (((uint64_t)c_hi << 32) | c_lo) : 0ULL;
         // candidates are cheap (1-2 stream words + a compare against the
-        // slot's own minimum); the threshold refresh (64 shared loads) is
-        // periodic -- a stale, larger tmax only admits more candidates
-        if (cand) pm64_candidates<EXPO>(cand, id, s_winv[le], (uint32_t)(c0 + le), k0, table);
-        if (++since >= 16 || (cand && !(tmax < 1e300))) {
-          tmax = pm64_tmax(table, k0);
+        // slot's own minimum); the threshold refresh is periodic -- a stale,
+        // larger tmax only admits more candidates
+        if (cand) pm64_candidates<EXPO>(cand, id, w, (uint32_t)e, t, tpg, table);
+        if (++since >= PM64_REFRESH || (cand && !(tmax < 1e300))) {
+          tmax = pm64_tmax(table, t, tpg);
           since = 0;
         }
+        // reconverge: lanes that took the candidate path would otherwise run
+        // the straight-line body out of phase (independent thread scheduling)
+        __syncwarp();
       }
     }
     __syncthreads();
     uint64_t* sig = a.sig + (size_t)s * m;
     for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-      const unsigned long long bi = table[k].idx;
+      const unsigned long long bi = table[pm64_slot(k / PM64_C, (int)(k % PM64_C), tpg)].idx;
       sig[k] = bi < (unsigned long long)n ? a.ids[off + bi] : 0ULL;
     }
     if (a.stats && threadIdx.x == 0) {

@@ -166,86 +166,77 @@ __device__ int warp_el_static(SetCtx& c, const Tables& T, WarpScratch& ws, int l
 
 // ---- labels without replacement: PMH2, PMH4, uw4 -------------------------
 
-// Lane 0 parses up to 32 points of the window: bit offsets, rejection draws
-// of the Fisher-Yates indices (uniform_int(m-i+1), K:225), the dense FY map
-// updates, and (PMH4) the TruncExp fast-path test / slow path.
-template <int F>
-__device__ void parse_fy_batch(SetCtx& c, const Tables& T, WarpScratch& ws, EpochFY fy,
-                               uint64_t id, uint64_t off, int64_t i0) {
+// Lane 0 parses up to 32 points of the window: the bit offset of each point's
+// value draw (53 bits) and its Fisher-Yates index r = uniform_int(m-pt+1)
+// (kbits-wide rejection rounds, K:97-117, K:225), assuming TruncExp's fast
+// path.  Only integer work is on this serial chain; the fast-path test, the
+// Fisher-Yates map steps and all floating point run afterwards.
+__device__ __forceinline__ uint32_t bits_for_fast(int64_t R) {  // == bits_for(R), R >= 2
+  return 64u - (uint32_t)__clzll((long long)(R - 1));
+}
+
+__device__ void parse_fy_cursor(const SetCtx& c, WarpScratch& ws, uint64_t id, uint64_t off,
+                                int64_t i0) {
   const int64_t m = c.m;
   const uint64_t wb = off >> 6;
   uint32_t cur = (uint32_t)(off - (wb << 6));
   uint32_t q = 0;
-  ws.flags = 0;
+  uint32_t flags = 0;
+  uint64_t next_off = 0;
   while (q < 32) {
     const int64_t pt = i0 + q;
-    if (pt > m) break;
-    if (cur + 53 > WIN_BITS) break;
+    if (pt > m || cur + 53 > WIN_BITS) break;
     const uint32_t eo = cur;
     uint32_t c2 = cur + 53;
-    double tv = __longlong_as_double(0x7FF8000000000000LL);  // NaN: Exp(1) draw
-    bool slow = false;
-    Stream st;
-    if (F == FAM_PMH4 && pt < m) {
-      const TruncExpConsts& cc = T.c4[pt];
-      const double t = cc.c1 * ((double)win_bits(ws.words, eo, 53) * INV53);
-      if (t < 1.0) {
-        tv = t;
-      } else {
-        st.seek(id, (wb << 6) + eo + 53);
-        bool fail = false;
-        tv = trunc_exp_slow(st, cc, &fail);
-        if (fail) { ws.flags = 2u; break; }
-        slow = true;
-      }
-    } else if (F == FAM_UW4) {
-      tv = (double)win_bits(ws.words, eo, 53) * INV53;  // the uniform itself
-    }
-    // Fisher-Yates index r = uniform_int(m - pt + 1)
     const int64_t R = m - pt + 1;
     int64_t r = 0;
     if (R > 1) {
-      const uint32_t kb = bits_for(R);
-      if (slow) {
+      const uint32_t kb = bits_for_fast(R);
+      int rounds = 0;
+      bool fits = true;
+      for (;;) {
+        if (c2 + kb > WIN_BITS) { fits = false; break; }
+        const uint64_t v = win_bits(ws.words, c2, kb);
+        c2 += kb;
+        if (v < (uint64_t)R) { r = (int64_t)v; break; }
+        if (++rounds > REJECT_CAP) { flags = 2u; break; }
+      }
+      if (flags) break;
+      if (!fits) {
+        if (q > 0) break;
+        // the first point of the batch does not fit the window: finish it
+        // with a sequential cursor and end the batch after it
+        Stream st;
+        st.seek(id, (wb << 6) + eo + 53);
         r = uniform_int_masked(st, (uint64_t)R, kb);
-        if (r < 0) { ws.flags = 2u; break; }
-      } else {
-        int rounds = 0;
-        bool fits = true;
-        for (;;) {
-          if (c2 + kb > WIN_BITS) { fits = false; break; }
-          const uint64_t v = win_bits(ws.words, c2, kb);
-          c2 += kb;
-          if (v < (uint64_t)R) { r = (int64_t)v; break; }
-          if (++rounds > REJECT_CAP) { ws.flags = 2u; break; }
-        }
-        if (ws.flags & 2u) break;
-        if (!fits) {
-          if (q > 0) break;
-          // the first point of the batch does not fit: finish it sequentially
-          st.seek(id, (wb << 6) + eo + 53);
-          r = uniform_int_masked(st, (uint64_t)R, kb);
-          if (r < 0) { ws.flags = 2u; break; }
-          slow = true;
-        }
+        if (r < 0) { flags = 2u; break; }
+        ws.eoff[q] = eo;
+        ws.lab[q] = (int32_t)r;
+        q++;
+        flags = 1u;
+        next_off = st.pos(id);
+        break;
       }
     }
-    const int32_t j = (int32_t)(pt + r);
-    const int32_t kj = fy.get(j);
-    fy.set(j, fy.get((int32_t)pt));
-    ws.lab[q] = kj;
     ws.eoff[q] = eo;
-    ws.tval[q] = tv;
+    ws.lab[q] = (int32_t)r;       // the FY index for now; the label after fy_steps
     q++;
-    if (slow) {
-      ws.flags = 1u;
-      ws.next_off = st.pos(id);
-      break;
-    }
     cur = c2;
   }
   ws.q = q;
-  if (!(ws.flags & 1u)) ws.next_off = (wb << 6) + cur;
+  ws.flags = flags;
+  ws.next_off = (flags & 1u) ? next_off : (wb << 6) + cur;
+}
+
+// lazy Fisher-Yates steps (K:222-235) for points i0 .. i0+q-1: r -> label
+__device__ __forceinline__ void fy_steps(WarpScratch& ws, EpochFY fy, int64_t i0, uint32_t q) {
+  for (uint32_t k = 0; k < q; k++) {
+    const int32_t pt = (int32_t)(i0 + k);
+    const int32_t j = pt + ws.lab[k];
+    const int32_t kj = fy.get(j);
+    fy.set(j, fy.get(pt));
+    ws.lab[k] = kj;
+  }
 }
 
 template <int F>
@@ -266,34 +257,66 @@ __device__ int warp_el_fy(SetCtx& c, const Tables& T, WarpScratch& ws, uint32_t*
   for (;;) {
     const uint64_t wb = off >> 6;
     win_load(ws, id, wb, lane);
-    if (lane == 0) parse_fy_batch<F>(c, T, ws, efy, id, off, i);
+    if (lane == 0) parse_fy_cursor(c, ws, id, off, i);
     __syncwarp();
     if (ws.flags & 2u) return EL_FAIL;
-    const uint32_t q = ws.q;
-    const double thr = warp_thr(c);
+    uint32_t q = ws.q;
     const int64_t pt = i + lane;
+    const bool in0 = (uint32_t)lane < q;
+    // value draw of this lane's point (fast path assumed by the parse)
+    const uint64_t u = in0 ? win_bits(ws.words, ws.eoff[lane], 53) : 0;
+    double tv = 0.0;
+    if constexpr (F == FAM_PMH4) {
+      bool slow = false;
+      if (in0 && pt < m) {
+        tv = __ldg(&T.c4[pt].c1) * ((double)u * INV53);
+        slow = !(tv < 1.0);
+      }
+      const unsigned sm = __ballot_sync(0xffffffffu, slow);
+      if (sm) {
+        const int f = __ffs(sm) - 1;
+        q = (uint32_t)f + 1;   // points after a slow draw have unknown offsets
+        if (lane == f) {
+          Stream st;
+          st.seek(id, (wb << 6) + ws.eoff[f] + 53);
+          bool fail = false;
+          tv = trunc_exp_slow(st, T.c4[pt], &fail);
+          const int64_t R = m - pt + 1;
+          const int64_t r = uniform_int_masked(st, (uint64_t)R, bits_for_fast(R));
+          ws.lab[f] = (int32_t)r;
+          ws.next_off = st.pos(id);
+          if (fail || r < 0) ws.flags = 2u;
+        }
+        __syncwarp();
+        if (ws.flags & 2u) return EL_FAIL;
+      }
+    } else if constexpr (F == FAM_UW4) {
+      tv = (double)u * INV53;  // the uniform itself
+    }
+    if (lane == 0) fy_steps(ws, efy, i, q);
+    __syncwarp();
+    const double thr = warp_thr(c);
     const bool in = (uint32_t)lane < q;
     double xv = 0.0;
     if constexpr (F == FAM_PMH2) {
       double d = 0.0;
       if (in) {
-        const double E = exp1_from_bits(win_bits(ws.words, ws.eoff[lane], 53));
+        const double E = exp1_from_bits(u);
         d = pt == 1 ? winv * E : (winv * __ldg(&T.beta[pt])) * E;
       }
       xv = ordered_fold(x, d, lane, q);
     } else if constexpr (F == FAM_PMH4) {
       if (in) {
         if (pt == 1) {
-          xv = winv * ws.tval[0];
+          xv = winv * tv;
         } else if (pt < m) {
-          xv = winv * (__ldg(&T.gam[pt - 1]) + __ldg(&T.dgam[pt]) * ws.tval[lane]);
+          xv = winv * (__ldg(&T.gam[pt - 1]) + __ldg(&T.dgam[pt]) * tv);
         } else {
-          const double E = exp1_from_bits(win_bits(ws.words, ws.eoff[lane], 53));
-          xv = winv * (__ldg(&T.gam[m - 1]) + T.delta * E);
+          xv = winv * (__ldg(&T.gam[m - 1]) + T.delta * exp1_from_bits(u));
         }
       }
     } else {  // uw4
-      if (in) xv = pt == 1 ? ws.tval[lane] : ((double)pt - 1.0) + ws.tval[lane];
+      if (in) xv = pt == 1 ? tv : ((double)pt - 1.0) + tv;
     }
     const bool valid = in && xv <= thr;
     const unsigned vm = __ballot_sync(0xffffffffu, valid);
