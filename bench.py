@@ -39,6 +39,12 @@ M = 1024
 VARIANTS = ["pminhash", "probminhash1", "probminhash1a", "probminhash2",
             "probminhash3", "probminhash3a", "probminhash4"]
 METRIC = "set elements hashed/sec at m=1024"
+# splitmix64 word: 64-bit add (2) + 3 x (64-bit shift + xor: 4) = 14 ALU ops;
+# a 53-bit draw uses 53/64 word, + 2 ops (extract 32 bits, compare)
+ALU_OPS_PER_DRAW = 14.0 * 53.0 / 64.0 + 2.0
+# dram read+write bytes per launch from `ncu --set full` of the full config-2
+# launch (profiles/r01_ncu_pminhash64_full.txt); None until captured
+TRAFFIC_BYTES = {"pminhash": 1447215000 + 34147328}
 UNIT = "elements/s"
 
 
@@ -303,15 +309,35 @@ def main():
     hbm_peak, peak_src = _peaks()
     dom = max(per_variant_ms, key=per_variant_ms.get)
     alg_bytes = algorithmic_bytes(N, S, M)
-    achieved = alg_bytes / (per_variant_ms[dom] / 1e3) / 1e9
-    roofline = {
-        "bound": "hbm", "kernel": f"sketch[{dom}]", "achieved": achieved, "peak": hbm_peak,
-        "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
-        "peak_source": peak_src,
-        "algorithmic_bytes": alg_bytes,
-        "note": "achieved = SURVEY §8d algorithmic bytes (16 B/elt + 8m B/set + 8 B/set) "
-                "per launch / mean CUDA-event launch time",
-    }
+    hbm_achieved = alg_bytes / (per_variant_ms[dom] / 1e3) / 1e9
+    gops = ctypes.c_double(0.0)
+    pms = ctypes.c_double(0.0)
+    _lib.check(L.pmh_probe_alu_peak(ctypes.byref(gops), ctypes.byref(pms)))
+    if dom == "pminhash":
+        # ncu: the P-MinHash kernel is bound by the 32-bit ALU pipe.  Algorithmic
+        # ALU work = N*m draws x ALU_OPS_PER_DRAW (splitmix64: 64-bit add + three
+        # 64-bit xor-shifts = 14 ALU ops per word, 53/64 word per 53-bit draw,
+        # + 2 ops to extract and compare the draw; the two 64-bit multiplies run
+        # on the FMA pipe) -- see DESIGN.md §4.
+        alu_ops = float(N) * M * ALU_OPS_PER_DRAW
+        achieved = alu_ops / (per_variant_ms[dom] / 1e3) / 1e9
+        roofline = {
+            "bound": "alu", "kernel": "pminhash64_kernel", "achieved": achieved,
+            "peak": gops.value, "unit": "Gop/s (32-bit ALU pipe)",
+            "frac": achieved / gops.value, "traffic": TRAFFIC_BYTES.get(dom),
+            "peak_source": "measured live: pmh_probe_alu_peak (LOP3 chains, full occupancy)",
+            "algorithmic_ops": alu_ops, "ops_per_draw": ALU_OPS_PER_DRAW,
+            "hbm": {"achieved_GBps": hbm_achieved, "peak_GBps": hbm_peak,
+                    "frac": hbm_achieved / hbm_peak, "peak_source": peak_src,
+                    "algorithmic_bytes": alg_bytes},
+        }
+    else:
+        roofline = {
+            "bound": "hbm", "kernel": f"sketch[{dom}]", "achieved": hbm_achieved,
+            "peak": hbm_peak, "unit": "GB/s", "frac": hbm_achieved / hbm_peak,
+            "traffic": TRAFFIC_BYTES.get(dom), "peak_source": peak_src,
+            "algorithmic_bytes": alg_bytes,
+        }
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -328,7 +354,9 @@ def main():
         "per_variant_elems_per_s": {v: N / (t / 1e3) for v, t in per_variant_ms.items()},
         "e2e": {"value": world * len(variants) * N / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": len(variants) * args.steps,
+        # per variant call: 3 ordering kernels + the sketch kernel (+ the
+        # concurrent small-set kernel for the ProbMinHash families)
+        "gpu_launches": args.steps * sum(4 if v == "pminhash" else 5 for v in variants),
         "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),

@@ -120,6 +120,13 @@ int pmh_allpairs_tile(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0,
 int pmh_bbit(const uint64_t* sig, int64_t nsets, int64_t m, int b,
              int64_t* out, void* stream);
 
+/*
+ * Diagnostic: measured 32-bit ALU-pipe peak of the current device in Gop/s
+ * (8 independent LOP3 chains per thread, full occupancy) -- the roofline
+ * denominator for the integer-bound signature kernels.  Synchronous.
+ */
+int pmh_probe_alu_peak(double* gops_out, double* ms_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,7 +13,7 @@ import threading
 from .errors import EmptyInputError, InvalidParamsError, RandomnessFailureError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpmh.so")
+LIB_PATH = os.environ.get("PMH_LIB_PATH") or os.path.join(_HERE, "libpmh.so")
 
 PMH_OK = 0
 PMH_ERR_EMPTY = -1
@@ -35,7 +35,7 @@ UNWEIGHTED_IDS = {10, 11, 12, 13, 14, 15, 16, 17, 18}
 # every symbol include/pmh.h declares
 EXPORTS = ("pmh_version", "pmh_last_error", "pmh_sketch_csr", "pmh_sketch_csr_async",
            "pmh_status_reset", "pmh_status_check", "pmh_sketch_csr_host",
-           "pmh_count_equal", "pmh_allpairs_tile", "pmh_bbit")
+           "pmh_count_equal", "pmh_allpairs_tile", "pmh_bbit", "pmh_probe_alu_peak")
 
 _lib = None
 _lock = threading.Lock()
@@ -82,6 +82,9 @@ def load():
         L.pmh_allpairs_tile.restype = ctypes.c_int
         L.pmh_bbit.argtypes = [_vp, _i64, _i64, ctypes.c_int, _vp, _vp]
         L.pmh_bbit.restype = ctypes.c_int
+        L.pmh_probe_alu_peak.argtypes = [ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double)]
+        L.pmh_probe_alu_peak.restype = ctypes.c_int
         _lib = L
         return L
 

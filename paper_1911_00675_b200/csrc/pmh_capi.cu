@@ -21,6 +21,8 @@
 #include "pmh_pminhash.cuh"
 #include "pmh_kernel.cuh"
 #include "pmh_order.cuh"
+#include "pmh_probe.cuh"
+#include "pmh_baselines.cuh"
 
 using namespace pmh;
 
@@ -252,14 +254,15 @@ cudaError_t launch_small(const SketchArgs& a, cudaStream_t st) {
 
 // argument validation with the reference's error domain (sketch.py:96-114);
 // runs before any CUDA call
+bool is_baseline(int algo) { return algo == ALG_SUPERMINHASH || algo == ALG_OPH; }
+
 int validate_sketch(int algo, int64_t m, const double* weights, int64_t nsets) {
   const int fam = family_of(algo);
-  if (algo != ALG_PMINHASH && algo != ALG_MINHASH && fam == 0)
+  if (algo != ALG_PMINHASH && algo != ALG_MINHASH && !is_baseline(algo) && fam == 0)
     return set_error(PMH_ERR_INVALID, "unsupported algorithm id " + std::to_string(algo));
   if (m < min_m(algo))
     return set_error(PMH_ERR_INVALID, "signature size must be >= " + std::to_string(min_m(algo)));
-  if (algo != ALG_PMINHASH && algo != ALG_MINHASH &&
-      sketch_smem_bytes(fam, m, SKETCH_THREADS) > 227 * 1024)
+  if (fam != 0 && sketch_smem_bytes(fam, m, SKETCH_THREADS) > 227 * 1024)
     return set_error(PMH_ERR_INVALID, "signature size too large for the shared-memory slot table");
   if ((algo == ALG_PMINHASH || algo == ALG_MINHASH) && m > 64LL * PMIN_THREADS)
     return set_error(PMH_ERR_INVALID, "signature size too large for the P-MinHash kernel");
@@ -315,6 +318,29 @@ int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
   long long* d_err_set = reinterpret_cast<long long*>(d_status + 1);
 
   cudaError_t e;
+  if (is_baseline(algo)) {
+    BaseArgs b{ids, offsets, nsets, m, sig_out, stats_out, d_err_set, flags};
+    const int64_t grid = nsets < 2147483647LL ? nsets : 2147483647LL;
+    if (algo == ALG_OPH) {
+      const size_t smem = sizeof(Slot) * (size_t)m;
+      PMH_CUDA(cudaFuncSetAttribute(oph_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      oph_kernel<<<(unsigned)grid, 256, smem, st>>>(b);
+    } else {
+      int threads = 256;
+      size_t smem = sizeof(Slot) * (size_t)m + sizeof(int32_t) * (size_t)m * (threads / 32);
+      while (smem > 200 * 1024 && threads > 32) {
+        threads /= 2;
+        smem = sizeof(Slot) * (size_t)m + sizeof(int32_t) * (size_t)m * (threads / 32);
+      }
+      if (smem > 227 * 1024) return set_error(PMH_ERR_INVALID, "signature size too large");
+      PMH_CUDA(cudaFuncSetAttribute(superminhash_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      superminhash_kernel<<<(unsigned)grid, threads, smem, st>>>(b);
+    }
+    PMH_CUDA(cudaGetLastError());
+    return PMH_OK;
+  }
   const bool pmin = algo == ALG_PMINHASH || algo == ALG_MINHASH;
   OrderWs ow;
   // cost offset: ProbMinHash families pay ~m ln m points per set regardless of n
@@ -325,7 +351,7 @@ int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
   void* order_ws = ow.mem;
   if (pmin) {
     PMinArgs a{ids, algo == ALG_PMINHASH ? weights : nullptr, offsets, order, nsets, m,
-               sig_out, stats_out, d_err_set};
+               sig_out, stats_out, d_err_set, 4u};
     e = algo == ALG_PMINHASH ? launch_pminhash<true>(a, st) : launch_pminhash<false>(a, st);
   } else {
     const Tables* tp = nullptr;
@@ -485,4 +511,31 @@ int pmh_bbit(const uint64_t* sig, int64_t nsets, int64_t m, int b, int64_t* out,
   return PMH_OK;
 }
 
+int pmh_probe_alu_peak(double* gops_out, double* ms_out) {
+  int dev = 0, sms = 0;
+  PMH_CUDA(cudaGetDevice(&dev));
+  PMH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  uint32_t* d = nullptr;
+  PMH_CUDA(cudaMalloc(&d, 16));
+  cudaEvent_t a, b;
+  PMH_CUDA(cudaEventCreate(&a));
+  PMH_CUDA(cudaEventCreate(&b));
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  alu_probe_kernel<<<blocks, threads>>>(16, d);  // warm-up
+  PMH_CUDA(cudaEventRecord(a));
+  alu_probe_kernel<<<blocks, threads>>>(iters, d);
+  PMH_CUDA(cudaEventRecord(b));
+  PMH_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  PMH_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(d);
+  const double ops = (double)blocks * threads * iters * 16.0 * 8.0;
+  if (gops_out) *gops_out = ops / (ms * 1e-3) / 1e9;
+  if (ms_out) *ms_out = ms;
+  return PMH_OK;
+}
+
 }  // extern "C"
+

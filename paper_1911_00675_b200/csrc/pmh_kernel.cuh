@@ -25,8 +25,11 @@ __host__ __device__ inline size_t sketch_smem_bytes(int family, int64_t m, int t
 }
 
 // Dynamic shared memory: Slot[m] | WarpScratch[nwarps] | int32 FY[nwarps][m+1]
+#ifndef SKETCH_MINBLOCKS
+#define SKETCH_MINBLOCKS 2
+#endif
 template <int F>
-__global__ void __launch_bounds__(SKETCH_THREADS) sketch_sets_kernel(SketchArgs a) {
+__global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS) sketch_sets_kernel(SketchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_hmax;
   __shared__ unsigned int s_filled;
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(SKETCH_THREADS) sketch_sets_kernel(SketchArgs 
     c.m = m;
     c.kbits = bits_for(m);
     c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
-    c.points = 0; c.updates = 0; c.multi = 0;
+    c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0;
     double tg = (double)m * (log((double)m) + a.tconst) / W;
     if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
     bool failed = false;
@@ -149,6 +152,7 @@ __global__ void __launch_bounds__(SKETCH_THREADS) sketch_sets_kernel(SketchArgs 
       const int any_fail = __syncthreads_or(failed ? 1 : 0);
       if (any_fail) { failed = true; break; }
       if (!s_retry) break;
+      c.tprev = tg;
       tg = attempt >= 2 ? __longlong_as_double(0x7FF0000000000000LL) : tg * 4.0;
       __syncthreads();
     }
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
     c.m = m;
     c.kbits = bits_for(m);
     c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
-    c.points = 0; c.updates = 0; c.multi = 0;
+    c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0;
     double tg = (double)m * (log((double)m) + a.tconst) / W;
     if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
     bool failed = false;
@@ -283,6 +287,7 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
         mx = v > mx ? v : mx;
       }
       if (failed || !(__longlong_as_double((long long)mx) > tg)) break;
+      c.tprev = tg;
       tg = attempt >= 2 ? __longlong_as_double(0x7FF0000000000000LL) : tg * 4.0;
     }
     if (failed && lane == 0) {

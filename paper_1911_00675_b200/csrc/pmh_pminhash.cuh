@@ -28,6 +28,7 @@ struct PMinArgs {
   uint64_t* sig;
   int64_t* stats;
   long long* err_set;
+  uint32_t k4;              // == 4, opaque to the compiler (see mix64_bal)
 };
 
 constexpr int PMIN_THREADS = 256;
@@ -231,8 +232,11 @@ __device__ __forceinline__ double pm64_tmax(const Slot* table, int64_t t, int tp
 // Each group of tpg = m/64 threads walks its elements g, g + G, ... straight
 // from global memory (broadcast loads, next element prefetched): no block
 // barrier inside a set, so warps with more candidates do not stall the CTA.
+#ifndef PM64_MINBLOCKS
+#define PM64_MINBLOCKS 4   // 64 registers, 4 CTAs (32 warps) per SM
+#endif
 template <bool EXPO>
-__global__ void __launch_bounds__(PMIN_THREADS) pminhash64_kernel(PMinArgs a) {
+__global__ void __launch_bounds__(PMIN_THREADS, PM64_MINBLOCKS) pminhash64_kernel(PMinArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int64_t m = a.m;
   const int tpg = (int)(m / PM64_C);               // threads per group
@@ -284,6 +288,7 @@ __global__ void __launch_bounds__(PMIN_THREADS) pminhash64_kernel(PMinArgs a) {
                                                       : 0xFFFFFFFFu;
         uint64_t st = id + wbase * GOLDEN;
         uint32_t c_lo = 0, c_hi = 0;
+        const uint32_t k4 = a.k4;
 #include "pm64_body.inc"
         const uint64_t cand = live ? (((uint64_t)c_hi << 32) | c_lo) : 0ULL;
         // candidates are cheap (1-2 stream words + a compare against the

@@ -46,6 +46,8 @@ struct SetCtx {
   int64_t cap;                       // coupon cap K:279-281
   // counters (per thread)
   int64_t points;
+  double tprev;                      // previous attempt's threshold (-1: none);
+                                     // a retry counts only points above it
   int64_t updates;
   int64_t multi;                     // elements that produced > 1 point
 };
@@ -156,7 +158,7 @@ __device__ __forceinline__ int el_pmh1(SetCtx& c, int64_t e, uint64_t id,
                                        double winv) {
   Stream st; st.seed(id);
   uint64_t b = st.next53();
-  c.points++;
+  c.points += (0.0 > c.tprev);  // first point: LB = 0
   if (exp1_scaled_lower_bound(winv, b) > ctx_thr(c)) return EL_DONE;
   double x = winv * exp1_from_bits(b);
   int64_t cnt = 1;
@@ -165,7 +167,7 @@ __device__ __forceinline__ int el_pmh1(SetCtx& c, int64_t e, uint64_t id,
     if (r < 0) return EL_FAIL;
     ctx_offer(c, r, x, e);
     b = st.next53();
-    c.points++;
+    c.points += (x > c.tprev);
     if (cnt == 1) c.multi++;
     if (++cnt > c.cap) return EL_FAIL;
     if (x + exp1_scaled_lower_bound(winv, b) > ctx_thr(c)) return EL_DONE;
@@ -180,7 +182,7 @@ __device__ __forceinline__ int el_pmh2(SetCtx& c, const Tables& T, FY& fy,
                                        int64_t e, uint64_t id, double winv) {
   Stream st; st.seed(id);
   uint64_t b = st.next53();
-  c.points++;
+  c.points += (0.0 > c.tprev);  // first point: LB = 0
   if (exp1_scaled_lower_bound(winv, b) > ctx_thr(c)) return EL_DONE;
   double x = winv * exp1_from_bits(b);
   int64_t i = 1;
@@ -192,7 +194,7 @@ __device__ __forceinline__ int el_pmh2(SetCtx& c, const Tables& T, FY& fy,
     if (i > c.m) break;
     const double a = winv * __ldg(&T.beta[i]);
     b = st.next53();
-    c.points++;
+    c.points += (x > c.tprev);
     if (i == 2) c.multi++;
     if (x + exp1_scaled_lower_bound(a, b) > ctx_thr(c)) return EL_DONE;
     x = x + a * exp1_from_bits(b);
@@ -206,7 +208,7 @@ __device__ __forceinline__ int el_pmh3(SetCtx& c, const Tables& T, int64_t e,
   Stream st; st.seed(id);
   bool fail = false;
   double x = winv * trunc_exp(st, T.c3, &fail);
-  c.points++;
+  c.points += (0.0 > c.tprev);  // first point: LB = 0
   int64_t i = 1;
   while (x <= ctx_thr(c)) {
     int64_t r = uniform_int_masked(st, (uint64_t)c.m, c.kbits);
@@ -216,7 +218,7 @@ __device__ __forceinline__ int el_pmh3(SetCtx& c, const Tables& T, int64_t e,
     x = winv * ((double)i - 1.0);
     if (x > ctx_thr(c)) break;
     x = x + winv * trunc_exp(st, T.c3, &fail);
-    c.points++;
+    c.points += (winv * ((double)i - 1.0) > c.tprev);
     if (i == 2) c.multi++;
   }
   return fail ? EL_FAIL : EL_DONE;
@@ -229,7 +231,7 @@ __device__ __forceinline__ int el_pmh4(SetCtx& c, const Tables& T, FY& fy,
   Stream st; st.seed(id);
   bool fail = false;
   double x = winv * trunc_exp(st, T.c4[1], &fail);
-  c.points++;
+  c.points += (0.0 > c.tprev);  // first point: LB = 0
   int64_t i = 1;
   const int64_t m = c.m;
   while (x <= ctx_thr(c)) {
@@ -243,10 +245,10 @@ __device__ __forceinline__ int el_pmh4(SetCtx& c, const Tables& T, FY& fy,
     if (i < m) {
       const double t = trunc_exp(st, T.c4[i], &fail);
       x = winv * (__ldg(&T.gam[i - 1]) + __ldg(&T.dgam[i]) * t);
-      c.points++;
+      c.points += (winv * __ldg(&T.gam[i - 1]) > c.tprev);
     } else {
       x = winv * (__ldg(&T.gam[m - 1]) + T.delta * exp1_from_bits(st.next53()));
-      c.points++;
+      c.points += (winv * __ldg(&T.gam[i - 1]) > c.tprev);
       if (x <= ctx_thr(c)) {
         k = perm_next(st, fy, m, m);
         if (k <= 0) return k == 0 ? EL_NEED_WARP : EL_FAIL;
@@ -262,7 +264,7 @@ __device__ __forceinline__ int el_pmh4(SetCtx& c, const Tables& T, FY& fy,
 __device__ __forceinline__ int el_uw3(SetCtx& c, int64_t e, uint64_t id) {
   Stream st; st.seed(id);
   double x = st.uniform01();
-  c.points++;
+  c.points += (0.0 > c.tprev);  // first point: LB = 0
   int64_t i = 1;
   while (x <= ctx_thr(c)) {
     int64_t r = uniform_int_masked(st, (uint64_t)c.m, c.kbits);
@@ -272,7 +274,7 @@ __device__ __forceinline__ int el_uw3(SetCtx& c, int64_t e, uint64_t id) {
     x = (double)i - 1.0;
     if (x > ctx_thr(c)) break;
     x = x + st.uniform01();
-    c.points++;
+    c.points += (((double)i - 1.0) > c.tprev);
     if (i == 2) c.multi++;
   }
   return EL_DONE;
@@ -283,7 +285,7 @@ template <class FY>
 __device__ __forceinline__ int el_uw4(SetCtx& c, FY& fy, int64_t e, uint64_t id) {
   Stream st; st.seed(id);
   double x = st.uniform01();
-  c.points++;
+  c.points += (0.0 > c.tprev);  // first point: LB = 0
   int64_t i = 1;
   const int64_t m = c.m;
   while (x <= ctx_thr(c)) {
@@ -295,10 +297,10 @@ __device__ __forceinline__ int el_uw4(SetCtx& c, FY& fy, int64_t e, uint64_t id)
     if (i == 2) c.multi++;
     if (i < m) {
       x = ((double)i - 1.0) + st.uniform01();
-      c.points++;
+      c.points += (((double)i - 1.0) > c.tprev);
     } else {
       x = ((double)m - 1.0) + st.uniform01();
-      c.points++;
+      c.points += (((double)i - 1.0) > c.tprev);
       if (x <= ctx_thr(c)) {
         k = perm_next(st, fy, m, m);
         if (k <= 0) return k == 0 ? EL_NEED_WARP : EL_FAIL;

@@ -153,7 +153,9 @@ __device__ int warp_el_static(SetCtx& c, const Tables& T, WarpScratch& ws, int l
     const bool trig = valid ? offer_trig(c, lab - 1, xv, e) : false;
     if (__any_sync(0xffffffffu, trig)) hmax_refresh_warp(c, lane);
     const uint32_t nv = __popc(vm);
-    if (lane == 0) c.points += nv + (nv < ncand ? 1 : 0);
+    // a retry attempt only counts points above the previous threshold
+    const uint32_t nn = __popc(__ballot_sync(0xffffffffu, cand && !(xv <= c.tprev)));
+    if (lane == 0) c.points += (c.tprev < 0.0 ? nv + (nv < ncand ? 1 : 0) : nn);
     if (nv < ncand) return EL_DONE;
     i += ncand;
     if (i > c.cap) return EL_FAIL;
@@ -323,7 +325,8 @@ __device__ int warp_el_fy(SetCtx& c, const Tables& T, WarpScratch& ws, uint32_t*
     const bool trig = valid ? offer_trig(c, ws.lab[lane] - 1, xv, e) : false;
     if (__any_sync(0xffffffffu, trig)) hmax_refresh_warp(c, lane);
     const uint32_t nv = __popc(vm);
-    if (lane == 0) c.points += nv + (nv < q ? 1 : 0);
+    const uint32_t nn = __popc(__ballot_sync(0xffffffffu, in && !(xv <= c.tprev)));
+    if (lane == 0) c.points += (c.tprev < 0.0 ? nv + (nv < q ? 1 : 0) : nn);
     if (nv < q) return EL_DONE;
     i += q;
     if (i > m) return EL_DONE;

@@ -9,7 +9,7 @@ pytestmark = pytest.mark.gpu
 
 GPU_ALGOS = {"pminhash", "probminhash1", "probminhash1a", "probminhash2", "probminhash3",
              "probminhash3a", "probminhash4", "unweighted1", "unweighted1a", "unweighted2",
-             "unweighted3", "unweighted3a", "unweighted4", "minhash"}
+             "unweighted3", "unweighted3a", "unweighted4", "minhash", "superminhash", "oph"}
 
 
 def _gpu_sig(algo, m, batch):
