@@ -94,6 +94,17 @@ int pmh_status_reset(int64_t* d_status, void* stream);
 int pmh_status_check(const int64_t* d_status, int64_t* err_set, void* stream);
 
 /* Same with HOST buffers (pageable or pinned); nelems = offsets[nsets]. */
+/*
+ * Several algorithms over one host batch: the inputs cross PCIe once, in
+ * set-chunks that the first algorithm consumes as they land; each algorithm's
+ * signatures (sig_outs[k], host uint64[nsets*m]) and optional stats
+ * (stats_outs[k] or NULL) are copied back while the next one computes.
+ * Host-side empties are reported before any copy (EmptyInputError, *err_set).
+ */
+int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uint64_t* ids,
+                              const double* weights, const int64_t* offsets, int64_t nsets,
+                              int64_t nelems, uint64_t* const* sig_outs,
+                              int64_t* const* stats_outs, int64_t* err_set);
 int pmh_sketch_csr_host(int algo, int64_t m, const uint64_t* ids,
                         const double* weights, const int64_t* offsets,
                         int64_t nsets, int64_t nelems, uint64_t* sig_out,

@@ -34,7 +34,7 @@ UNWEIGHTED_IDS = {10, 11, 12, 13, 14, 15, 16, 17, 18}
 
 # every symbol include/pmh.h declares
 EXPORTS = ("pmh_version", "pmh_last_error", "pmh_sketch_csr", "pmh_sketch_csr_async",
-           "pmh_status_reset", "pmh_status_check", "pmh_sketch_csr_host",
+           "pmh_status_reset", "pmh_status_check", "pmh_sketch_csr_host", "pmh_sketch_csr_host_multi",
            "pmh_count_equal", "pmh_allpairs_tile", "pmh_bbit", "pmh_probe_alu_peak")
 
 _lib = None
@@ -75,6 +75,9 @@ def load():
         L.pmh_sketch_csr_host.argtypes = [ctypes.c_int, _i64, _vp, _vp, _vp, _i64, _i64,
                                           _vp, _vp, _i64p]
         L.pmh_sketch_csr_host.restype = ctypes.c_int
+        L.pmh_sketch_csr_host_multi.argtypes = [_vp, ctypes.c_int, _i64, _vp, _vp, _vp, _i64,
+                                                _i64, _vp, _vp, _i64p]
+        L.pmh_sketch_csr_host_multi.restype = ctypes.c_int
         L.pmh_count_equal.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp]
         L.pmh_count_equal.restype = ctypes.c_int
         L.pmh_allpairs_tile.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _i64,

@@ -113,6 +113,31 @@ def sketch_csr(algo, m: int, ids, weights, offsets, want_stats=True):
     return sig, stats
 
 
+def sketch_csr_multi(algos, m: int, ids, weights, offsets, sig_outs=None, want_stats=False):
+    """Several algorithms over one host batch through pmh_sketch_csr_host_multi
+    (inputs cross PCIe once; D2H overlaps the next algorithm's compute).
+    sig_outs: optional preallocated host uint64 [S, m] arrays (pinned for
+    full overlap).  Returns (list of sig arrays, list of stats or None)."""
+    _torch()
+    aids = (ctypes.c_int * len(algos))(*[algo_id(a) for a in algos])
+    ids = np.ascontiguousarray(ids, np.uint64)
+    offsets = np.ascontiguousarray(offsets, np.int64)
+    w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    nsets = offsets.size - 1
+    if sig_outs is None:
+        sig_outs = [np.empty((nsets, m), np.uint64) for _ in algos]
+    stats = [np.empty((nsets, 3), np.int64) for _ in algos] if want_stats else None
+    sp = (ctypes.c_void_p * len(algos))(*[o.ctypes.data for o in sig_outs])
+    stp = (ctypes.c_void_p * len(algos))(*[o.ctypes.data for o in stats]) if stats else None
+    err = ctypes.c_int64(-1)
+    rc = _lib.load().pmh_sketch_csr_host_multi(
+        aids, len(algos), m, ids.ctypes.data, w.ctypes.data if w is not None else None,
+        offsets.ctypes.data, nsets, int(offsets[-1]) if nsets > 0 else 0, sp, stp,
+        ctypes.byref(err))
+    _lib.check(rc, err.value)
+    return sig_outs, stats
+
+
 def count_equal_device(a, b):
     """a, b: int64 CUDA tensors [P, m] -> int32 CUDA tensor [P] of equal counts."""
     torch = _torch()

@@ -213,6 +213,22 @@ cudaError_t build_order(const int64_t* offsets, int64_t nsets, int64_t c, int64_
   return cudaGetLastError();
 }
 
+// Keep the stream-ordered allocator's memory resident between calls (the
+// default release threshold 0 would unmap the workspace at every sync).
+std::map<int, bool> g_pool_set;
+void ensure_pool_retained() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_pool_set[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  g_pool_set[dev] = true;
+}
+
 // per-device auxiliary stream + events for the concurrent small-set kernel
 struct AuxStream {
   cudaStream_t s = nullptr;
@@ -418,6 +434,7 @@ int pmh_sketch_csr(int algo, int64_t m, const uint64_t* ids,
   int vrc = validate_sketch(algo, m, weights, nsets);
   if (vrc != PMH_OK) return vrc;
   if (nsets == 0) return PMH_OK;
+  ensure_pool_retained();
   int64_t* d_status = nullptr;
   PMH_CUDA(cudaMallocAsync((void**)&d_status, 16, st));
   int rc = pmh_status_reset(d_status, st);
@@ -429,47 +446,135 @@ int pmh_sketch_csr(int algo, int64_t m, const uint64_t* ids,
   return rc;
 }
 
+int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uint64_t* ids,
+                              const double* weights, const int64_t* offsets, int64_t nsets,
+                              int64_t nelems, uint64_t* const* sig_outs,
+                              int64_t* const* stats_outs, int64_t* err_set) {
+  if (err_set) *err_set = -1;
+  if (nalgos < 1 || !algos || !sig_outs) return set_error(PMH_ERR_INVALID, "no algorithms");
+  if (nsets < 0 || nelems < 0) return set_error(PMH_ERR_INVALID, "negative sizes");
+  bool any_weighted = false;
+  for (int k = 0; k < nalgos; k++) {
+    int vrc = validate_sketch(algos[k], m, weights, nsets);
+    if (vrc != PMH_OK) return vrc;
+    any_weighted |= !is_unweighted(algos[k]);
+  }
+  if (nsets == 0) return PMH_OK;
+  if (offsets[nsets] != nelems) return set_error(PMH_ERR_INVALID, "offsets[nsets] != nelems");
+  for (int64_t s = 0; s < nsets; s++)  // host buffers: report empties up front
+    if (offsets[s + 1] <= offsets[s]) {
+      if (err_set) *err_set = s;
+      return set_error(PMH_ERR_EMPTY, "cannot sketch an empty set (set " + std::to_string(s) + ")");
+    }
+  const bool weighted = any_weighted && weights;
+  ensure_pool_retained();
+  cudaStream_t st = nullptr, cin = nullptr, cout = nullptr;
+  PMH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  PMH_CUDA(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
+  PMH_CUDA(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
+  const size_t bi = sizeof(uint64_t) * (size_t)nelems, bw = weighted ? sizeof(double) * (size_t)nelems : 0,
+               bo = sizeof(int64_t) * (size_t)(nsets + 1), bs = sizeof(uint64_t) * (size_t)nsets * (size_t)m,
+               bst = sizeof(int64_t) * 3 * (size_t)nsets;
+  const bool want_stats = stats_outs != nullptr;
+  const size_t per_algo = bs + (want_stats ? bst : 0);
+  char* d = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&d, bi + bw + bo + 16 + per_algo * (size_t)nalgos + 64, st);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(st); cudaStreamDestroy(cin); cudaStreamDestroy(cout);
+    return cuda_fail(e, "cudaMallocAsync");
+  }
+  uint64_t* d_ids = (uint64_t*)d;
+  double* d_w = (double*)(d + bi);
+  int64_t* d_off = (int64_t*)(d + bi + bw);
+  int64_t* d_status = (int64_t*)(d + bi + bw + bo);
+  char* d_out = d + bi + bw + bo + 16;
+  int rc = PMH_OK;
+  std::vector<cudaEvent_t> evs;
+  auto mkev = [&]() {
+    cudaEvent_t ev = nullptr;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    evs.push_back(ev);
+    return ev;
+  };
+  // offsets + status first, then the element arrays in NC set-chunks on the
+  // copy-in stream; the first algorithm runs chunk by chunk as they land
+  // (CSR offsets are absolute, so a chunk is just offsets + s0)
+  e = cudaMemcpyAsync(d_off, offsets, bo, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) rc = cuda_fail(e, "H2D offsets");
+  if (rc == PMH_OK) rc = pmh_status_reset(d_status, st);
+  cudaEvent_t ev_meta = mkev();
+  cudaEventRecord(ev_meta, st);
+  cudaStreamWaitEvent(cin, ev_meta, 0);
+  const int NC = nsets >= 8 && nelems >= (1 << 20) ? 4 : 1;
+  std::vector<int64_t> cut(NC + 1, 0);
+  cut[NC] = nsets;
+  for (int c = 1; c < NC; c++) {  // element-balanced set boundaries
+    const int64_t target = nelems * c / NC;
+    int64_t lo = cut[c - 1], hi = nsets;
+    while (lo < hi) { const int64_t mid = (lo + hi) / 2; if (offsets[mid] < target) lo = mid + 1; else hi = mid; }
+    cut[c] = lo;
+  }
+  for (int c = 0; c < NC && rc == PMH_OK; c++) {
+    const int64_t e0 = offsets[cut[c]], e1 = offsets[cut[c + 1]];
+    if (e1 > e0) {
+      if ((e = cudaMemcpyAsync(d_ids + e0, ids + e0, sizeof(uint64_t) * (size_t)(e1 - e0),
+                               cudaMemcpyHostToDevice, cin)) != cudaSuccess ||
+          (weighted && (e = cudaMemcpyAsync(d_w + e0, weights + e0, sizeof(double) * (size_t)(e1 - e0),
+                                            cudaMemcpyHostToDevice, cin)) != cudaSuccess)) {
+        rc = cuda_fail(e, "H2D");
+        break;
+      }
+    }
+    cudaEvent_t ev = mkev();
+    cudaEventRecord(ev, cin);
+    cudaStreamWaitEvent(st, ev, 0);
+    const int64_t ns = cut[c + 1] - cut[c];
+    if (ns > 0) {
+      uint64_t* sig0 = (uint64_t*)d_out + (size_t)cut[c] * m;
+      int64_t* st0 = want_stats ? (int64_t*)(d_out + bs) + 3 * cut[c] : nullptr;
+      rc = pmh_sketch_csr_async(algos[0], m, d_ids, weighted ? d_w : nullptr, d_off + cut[c], ns,
+                                sig0, st0, d_status, st);
+    }
+  }
+  // remaining algorithms over the whole batch; each result's D2H overlaps the
+  // next algorithm's compute on the copy-out stream
+  for (int k = 0; k < nalgos && rc == PMH_OK; k++) {
+    char* outk = d_out + per_algo * (size_t)k;
+    if (k > 0)
+      rc = pmh_sketch_csr_async(algos[k], m, d_ids, weighted ? d_w : nullptr, d_off, nsets,
+                                (uint64_t*)outk, want_stats ? (int64_t*)(outk + bs) : nullptr,
+                                d_status, st);
+    if (rc != PMH_OK) break;
+    cudaEvent_t ev = mkev();
+    cudaEventRecord(ev, st);
+    cudaStreamWaitEvent(cout, ev, 0);
+    if ((e = cudaMemcpyAsync(sig_outs[k], outk, bs, cudaMemcpyDeviceToHost, cout)) != cudaSuccess ||
+        (want_stats && stats_outs[k] &&
+         (e = cudaMemcpyAsync(stats_outs[k], outk + bs, bst, cudaMemcpyDeviceToHost, cout)) != cudaSuccess)) {
+      rc = cuda_fail(e, "D2H");
+      break;
+    }
+  }
+  cudaEvent_t ev_end = mkev();
+  cudaEventRecord(ev_end, cout);
+  cudaStreamWaitEvent(st, ev_end, 0);
+  if (rc == PMH_OK) rc = pmh_status_check(d_status, err_set, st);
+  cudaFreeAsync(d, st);
+  e = cudaStreamSynchronize(st);
+  for (auto ev : evs) cudaEventDestroy(ev);
+  cudaStreamDestroy(st); cudaStreamDestroy(cin); cudaStreamDestroy(cout);
+  if (rc == PMH_OK && e != cudaSuccess) rc = cuda_fail(e, "sync");
+  return rc;
+}
+
 int pmh_sketch_csr_host(int algo, int64_t m, const uint64_t* ids,
                         const double* weights, const int64_t* offsets,
                         int64_t nsets, int64_t nelems, uint64_t* sig_out,
                         int64_t* stats_out, int64_t* err_set) {
-  if (nsets <= 0 || nelems < 0) {
-    if (nsets == 0) return PMH_OK;
-    return set_error(PMH_ERR_INVALID, "negative sizes");
-  }
-  cudaStream_t st;
-  PMH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  const bool weighted = !is_unweighted(algo) && weights;
-  const size_t bi = sizeof(uint64_t) * (size_t)nelems, bw = weighted ? sizeof(double) * (size_t)nelems : 0,
-               bo = sizeof(int64_t) * (size_t)(nsets + 1), bs = sizeof(uint64_t) * (size_t)nsets * (size_t)m,
-               bst = stats_out ? sizeof(int64_t) * 3 * (size_t)nsets : 0;
-  char* d = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&d, bi + bw + bo + bs + bst + 64, st);
-  if (e != cudaSuccess) { cudaStreamDestroy(st); return cuda_fail(e, "cudaMallocAsync"); }
-  uint64_t* d_ids = (uint64_t*)d;
-  double* d_w = (double*)(d + bi);
-  int64_t* d_off = (int64_t*)(d + bi + bw);
-  uint64_t* d_sig = (uint64_t*)(d + bi + bw + bo);
-  int64_t* d_stats = stats_out ? (int64_t*)(d + bi + bw + bo + bs) : nullptr;
-  int rc = PMH_OK;
-  if ((e = cudaMemcpyAsync(d_ids, ids, bi, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
-      (weighted && (e = cudaMemcpyAsync(d_w, weights, bw, cudaMemcpyHostToDevice, st)) != cudaSuccess) ||
-      (e = cudaMemcpyAsync(d_off, offsets, bo, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
-    rc = cuda_fail(e, "H2D");
-  }
-  if (rc == PMH_OK)
-    rc = pmh_sketch_csr(algo, m, d_ids, weighted ? d_w : nullptr, d_off, nsets, d_sig, d_stats,
-                        err_set, st);
-  if (rc == PMH_OK) {
-    if ((e = cudaMemcpyAsync(sig_out, d_sig, bs, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (stats_out && (e = cudaMemcpyAsync(stats_out, d_stats, bst, cudaMemcpyDeviceToHost, st)) != cudaSuccess))
-      rc = cuda_fail(e, "D2H");
-  }
-  cudaFreeAsync(d, st);
-  e = cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
-  if (rc == PMH_OK && e != cudaSuccess) rc = cuda_fail(e, "sync");
-  return rc;
+  uint64_t* const sigs[1] = {sig_out};
+  int64_t* const stats[1] = {stats_out};
+  return pmh_sketch_csr_host_multi(&algo, 1, m, ids, weights, offsets, nsets, nelems, sigs,
+                                   stats_out ? stats : nullptr, err_set);
 }
 
 int pmh_count_equal(const uint64_t* a, const uint64_t* b, int64_t npairs,

@@ -292,3 +292,18 @@ def test_empty_set_in_batch_reports_index():
     rc = L.pmh_sketch_csr(_lib.ALG["probminhash3"], 16, t_ids.data_ptr(), t_w.data_ptr(),
                           t_off.data_ptr(), 3, sig.data_ptr(), None, ctypes.byref(err), None)
     assert rc == _lib.PMH_ERR_EMPTY and err.value == 1
+
+
+def test_host_multi_matches_single_calls():
+    """pmh_sketch_csr_host_multi (chunked H2D, overlapped D2H) == per-algorithm
+    device calls, including the chunked first algorithm."""
+    from paper_1911_00675_b200.batch import sketch_csr_multi
+    b = datagen.random_sets(31, list(np.exp(np.linspace(0, 9.5, 40)).astype(int) + 1), "uniform")
+    algos = ["probminhash3", "pminhash", "probminhash2", "probminhash4", "probminhash1"]
+    sigs, stats = sketch_csr_multi(algos, 256, b.ids, b.weights, b.offsets, want_stats=True)
+    for a, sg in zip(algos, sigs):
+        ref, _ = orc.sketch_csr(a, 256, b.ids, b.weights, b.offsets, threads=16)
+        assert np.array_equal(sg, ref), a
+    with pytest.raises(EmptyInputError):
+        sketch_csr_multi(["probminhash1"], 16, np.arange(3, dtype=np.uint64), np.ones(3),
+                         np.array([0, 3, 3]))
