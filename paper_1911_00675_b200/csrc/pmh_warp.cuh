@@ -27,7 +27,8 @@ namespace pmh {
 constexpr uint32_t WIN_BITS = 2048;  // 32 words
 
 struct WarpScratch {
-  uint64_t words[33];   // window (+1 guard word)
+  uint64_t words[65];   // window (64 words for the parallel FY parse, +1 guard)
+  uint32_t acc[32];     // per-point label-acceptance masks (parallel FY parse)
   uint32_t eoff[32];    // window-relative bit offset of each point's first draw
   int32_t lab[32];      // 1-based labels
   double tval[32];      // TruncExp values (PMH4 parse), NaN => exponential draw
@@ -56,6 +57,15 @@ __device__ __forceinline__ uint64_t win_bits(const uint64_t* w, uint32_t rel, ui
   uint64_t v = w[i] >> sh;
   if (sh && sh + k > 64) v |= w[i + 1] << (64 - sh);
   return k == 64 ? v : (v & ((1ULL << k) - 1ULL));
+}
+
+constexpr uint32_t WIN2_BITS = 4096;  // 64 words
+
+__device__ __forceinline__ void win_load64(WarpScratch& ws, uint64_t id, uint64_t wb, int lane) {
+  ws.words[lane] = stream_word(id, wb + 1 + (uint64_t)lane);
+  ws.words[lane + 32] = stream_word(id, wb + 33 + (uint64_t)lane);
+  if (lane == 0) ws.words[64] = stream_word(id, wb + 65);
+  __syncwarp();
 }
 
 __device__ __forceinline__ void win_load(WarpScratch& ws, uint64_t id, uint64_t wb, int lane) {
@@ -230,6 +240,76 @@ __device__ void parse_fy_cursor(const SetCtx& c, WarpScratch& ws, uint64_t id, u
   ws.next_off = (flags & 1u) ? next_off : (wb << 6) + cur;
 }
 
+// Warp-parallel version of parse_fy_cursor.  For a run of points whose
+// Fisher-Yates range R = m - pt + 1 shares the label width kb, point k starts
+// at base_k + kb * Y_k, where base_k = rel0 + k (53 + kb) and Y_k is the number
+// of REJECTED label rounds of points 0..k-1.  Lane k records in a 24-bit mask
+// which of its candidate label draws (base_k + 53 + kb t, t = 0..23) would be
+// accepted (< R_k); a warp-uniform scan Y_{k+1} = Y_k + ctz(acc_k >> Y_k) then
+// fixes every offset (K:97-117 rejection semantics exactly).  Falls back to the
+// serial parse when the run is empty or a point rejects beyond the window.
+__device__ void parse_fy_parallel(const SetCtx& c, WarpScratch& ws, uint64_t id, uint64_t off,
+                                  int64_t i0, int lane) {
+  const int64_t m = c.m;
+  const uint64_t wb = off >> 6;
+  const uint32_t rel0 = (uint32_t)(off - (wb << 6));
+  const int64_t R0 = m - i0 + 1;
+  if (R0 <= 1) {  // the last point (pt = m) draws no label bits
+    if (lane == 0) {
+      ws.eoff[0] = rel0;
+      ws.lab[0] = 0;
+      ws.q = 1;
+      ws.flags = 0;
+      ws.next_off = off + 53;
+    }
+    __syncwarp();
+    return;
+  }
+  const uint32_t kb = bits_for_fast(R0);
+  const int64_t pt = i0 + lane;
+  const int64_t R = m - pt + 1;
+  // lanes of the same-width run (R > 1 and bits_for(R) == kb)
+  const bool inrun = R > 1 && bits_for_fast(R) == kb;
+  const unsigned runmask = __ballot_sync(0xffffffffu, inrun);
+  const uint32_t qmax = runmask == 0xffffffffu ? 32u : (uint32_t)(__ffs(~runmask) - 1);
+  const uint32_t base = rel0 + (uint32_t)lane * (53u + kb);
+  if ((uint32_t)lane < qmax) {
+    uint32_t acc = 0;
+#pragma unroll 4
+    for (uint32_t t = 0; t < 24; t++) {
+      const uint32_t pos = base + 53u + kb * t;
+      const uint64_t v = win_bits(ws.words, pos, kb);
+      acc |= (v < (uint64_t)R ? 1u : 0u) << t;
+    }
+    ws.acc[lane] = acc;
+  }
+  __syncwarp();
+  // warp-uniform scan over the acceptance masks
+  uint32_t Y = 0, myY = 0, mye = 0, q = qmax;
+  for (uint32_t k = 0; k < qmax; k++) {
+    const uint32_t a = Y < 24 ? ws.acc[k] >> Y : 0u;
+    if (a == 0) { q = k; break; }
+    const uint32_t e = (uint32_t)(__ffs(a) - 1);
+    if ((uint32_t)lane == k) { myY = Y; mye = e; }
+    Y += e;
+  }
+  if (q == 0) {  // the first point's label needs more rounds than the window: serial
+    if (lane == 0) parse_fy_cursor(c, ws, id, off, i0);
+    __syncwarp();
+    return;
+  }
+  if ((uint32_t)lane < q) {
+    ws.eoff[lane] = base + kb * myY;
+    ws.lab[lane] = (int32_t)win_bits(ws.words, base + 53u + kb * (myY + mye), kb);
+  }
+  if (lane == (int)q - 1) {
+    ws.q = q;
+    ws.flags = 0;
+    ws.next_off = (wb << 6) + base + 53u + kb * (myY + mye + 1u);
+  }
+  __syncwarp();
+}
+
 // lazy Fisher-Yates steps (K:222-235) for points i0 .. i0+q-1: r -> label
 __device__ __forceinline__ void fy_steps(WarpScratch& ws, EpochFY fy, int64_t i0, uint32_t q) {
   for (uint32_t k = 0; k < q; k++) {
@@ -258,9 +338,8 @@ __device__ int warp_el_fy(SetCtx& c, const Tables& T, WarpScratch& ws, uint32_t*
   double x = 0.0;
   for (;;) {
     const uint64_t wb = off >> 6;
-    win_load(ws, id, wb, lane);
-    if (lane == 0) parse_fy_cursor(c, ws, id, off, i);
-    __syncwarp();
+    win_load64(ws, id, wb, lane);
+    parse_fy_parallel(c, ws, id, off, i, lane);
     if (ws.flags & 2u) return EL_FAIL;
     uint32_t q = ws.q;
     const int64_t pt = i + lane;
