@@ -14,6 +14,33 @@
 namespace pmh {
 
 constexpr double HEAVY_POINTS = 8.0;   // expected points above which mode B runs
+
+// Division-free prefilter for the common case of large sets: decide from the
+// element's first stream word whether its FIRST point exceeds thr and the
+// SECOND point's lower bound does too, in which case the element contributes
+// nothing (exactly what the recurrence would conclude).  Weighted families
+// compare against thr * w with 2^-40 margins, which dominate every rounding in
+// x = fl(fl(1/w) * E) (E >= U for PMH1/2; T exact for PMH3/4), so a rejection
+// here is always a rejection there.  Returns false when unsure.
+template <int F>
+__device__ __forceinline__ bool first_point_rejects(const SetCtx& c, const Tables& T, uint64_t id,
+                                                    double w, double thr) {
+  const uint64_t b53 = mix64(id + GOLDEN) & ((1ULL << 53) - 1ULL);  // bits 0..52 = word 1
+  const double U = (double)b53 * INV53;
+  const double lo = 0.99999999999909051, hi = 1.0000000000009095;  // 1 -/+ 2^-40
+  if constexpr (F == FAM_UW3 || F == FAM_UW4) {
+    return U > thr && 1.0 > thr;                 // x = U, next lower bound 1
+  } else if constexpr (F == FAM_PMH1 || F == FAM_PMH2) {
+    // next point's lower bound is x itself (x_2 = x + winv E_2 >= x)
+    return U * lo > thr * w * hi;
+  } else {
+    const double c1 = (F == FAM_PMH3) ? T.c3.c1 : T.c4[1].c1;
+    const double t = c1 * U;                     // TruncExp fast path (K:130-132)
+    if (!(t < 1.0)) return false;
+    // x = winv t; next lower bound winv * 1 (PMH3: winv * (2 - 1); PMH4: winv * gamma_1 = winv)
+    return t * lo > thr * w * hi && 1.0 * lo > thr * w * hi;
+  }
+}
 constexpr int SKETCH_THREADS = 256;
 
 __host__ __device__ inline size_t sketch_smem_bytes(int family, int64_t m, int threads) {
@@ -74,9 +101,18 @@ __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS) sketch_sets_
     }
     double W;
     if (family_weighted(F) && w) {
-      double part = 0.0;
-      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) part += w[e];
-      W = block_sum(part, s_red);
+      // four independent loads in flight per thread (latency-bound otherwise)
+      double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+      const int64_t B = blockDim.x;
+      int64_t e = threadIdx.x;
+      for (; e + 3 * B < n; e += 4 * B) {
+        p0 += __ldg(&w[e]);
+        p1 += __ldg(&w[e + B]);
+        p2 += __ldg(&w[e + 2 * B]);
+        p3 += __ldg(&w[e + 3 * B]);
+      }
+      for (; e < n; e += B) p0 += __ldg(&w[e]);
+      W = block_sum((p0 + p1) + (p2 + p3), s_red);
     } else {
       W = (double)n;
     }
@@ -100,40 +136,97 @@ __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS) sketch_sets_
       c.tguess = tg;
       if (threadIdx.x == 0) s_next = 0;
       __syncthreads();
-      for (;;) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(&s_next, (unsigned)chunk);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if ((int64_t)base >= n) break;
+      // Chunks of 32 elements are pulled from a shared counter; the next
+      // chunk's ids/weights are loaded before the current one is processed
+      // (global-load latency overlaps the work).  Every element first runs the
+      // division-free first-point prefilter; SURVIVORS are compacted into a
+      // per-warp queue and run through the full recurrence 32 at a time, so
+      // the expensive path executes with full warps instead of the few lanes
+      // that survive in any one chunk (large sets keep only ~1-15%).
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(&s_next, (unsigned)chunk);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      uint64_t id_nx = 0;
+      double w_nx = 1.0;
+      {
         const int64_t e = (int64_t)base + lane;
-        const bool active = lane < chunk && e < n;
-        uint64_t id = 0;
-        double winv = 1.0;
-        bool heavy = false;
-        int status = EL_DONE;
-        if (active) {
-          id = ids[e];
-          if (family_weighted(F) && w) winv = 1.0 / w[e];
-          heavy = warp_ok && ctx_thr(c) > HEAVY_POINTS * winv;
-          if (!heavy) {
-            SparseFY fy; fy.reset();
-            status = run_element<F>(c, a.T, fy, e, id, winv);
-          }
+        if (lane < chunk && e < n) {
+          id_nx = __ldg(&ids[e]);
+          if (family_weighted(F) && w) w_nx = __ldg(&w[e]);
         }
-        if (status == EL_FAIL) failed = true;
-        unsigned hm = __ballot_sync(0xffffffffu, active && (heavy || status == EL_NEED_WARP));
-        while (hm) {
-          const int l = __ffs(hm) - 1;
-          hm &= hm - 1;
-          const int64_t eh = __shfl_sync(0xffffffffu, e, l);
-          const uint64_t idh = __shfl_sync(0xffffffffu, id, l);
-          const double winvh = __shfl_sync(0xffffffffu, winv, l);
-          const int st = warp_element<F>(c, a.T, *wscr, fy_dense, lane, eh, idh, winvh);
-          if (st == EL_FAIL) failed = true;
-          if (lane == 0) c.multi++;
+      }
+      int since_refresh = 0;
+      int qn = 0;                                  // queued survivors (warp-uniform)
+      for (;;) {
+        const bool more = (int64_t)base < n;
+        if (more) {
+          const int64_t e = (int64_t)base + lane;
+          const bool active = lane < chunk && e < n;
+          const uint64_t id = id_nx;
+          const double wv = w_nx;
+          unsigned nbase = 0;
+          if (lane == 0) nbase = atomicAdd(&s_next, (unsigned)chunk);
+          nbase = __shfl_sync(0xffffffffu, nbase, 0);
+          const int64_t en = (int64_t)nbase + lane;
+          if (lane < chunk && en < n) {
+            id_nx = __ldg(&ids[en]);
+            if (family_weighted(F) && w) w_nx = __ldg(&w[en]);
+          }
+          bool surv = false;
+          if (active) {
+            surv = !first_point_rejects<F>(c, a.T, id, wv, ctx_thr(c));
+            if (!surv) c.points += (0.0 > c.tprev);          // rejected first point
+          }
+          const unsigned sm = __ballot_sync(0xffffffffu, surv);
+          if (surv) wscr->sq[qn + __popc(sm & ((1u << lane) - 1u))] = (int32_t)e;
+          qn += __popc(sm);
+          base = nbase;
           __syncwarp();
         }
-        hmax_refresh_warp(c, lane);
+        if (qn >= 32 || (!more && qn > 0)) {
+          // run up to 32 queued survivors, one per lane
+          const int take = qn < 32 ? qn : 32;
+          const bool act = lane < take;
+          const int64_t e = act ? (int64_t)wscr->sq[lane] : 0;
+          __syncwarp();
+          if (qn > 32 && lane < qn - 32) wscr->sq[lane] = wscr->sq[lane + 32];
+          qn -= take;
+          __syncwarp();
+          const int64_t upd0 = c.updates;
+          uint64_t id = 0;
+          double winv = 1.0;
+          bool heavy = false;
+          int status = EL_DONE;
+          if (act) {
+            id = __ldg(&ids[e]);
+            if (family_weighted(F) && w) winv = 1.0 / __ldg(&w[e]);
+            heavy = warp_ok && ctx_thr(c) > HEAVY_POINTS * winv;
+            if (!heavy) {
+              SparseFY fy; fy.reset();
+              status = run_element<F>(c, a.T, fy, e, id, winv);
+            }
+          }
+          if (status == EL_FAIL) failed = true;
+          unsigned hm = __ballot_sync(0xffffffffu, act && (heavy || status == EL_NEED_WARP));
+          while (hm) {
+            const int l = __ffs(hm) - 1;
+            hm &= hm - 1;
+            const int64_t eh = __shfl_sync(0xffffffffu, e, l);
+            const uint64_t idh = __shfl_sync(0xffffffffu, id, l);
+            const double winvh = __shfl_sync(0xffffffffu, winv, l);
+            const int st = warp_element<F>(c, a.T, *wscr, fy_dense, lane, eh, idh, winvh);
+            if (st == EL_FAIL) failed = true;
+            if (lane == 0) c.multi++;
+            __syncwarp();
+          }
+          // refresh h_max after batches that lowered a slot (and every 8th)
+          const bool changed = __any_sync(0xffffffffu, c.updates != upd0);
+          if (changed || ++since_refresh >= 8) {
+            hmax_refresh_warp(c, lane);
+            since_refresh = 0;
+          }
+        }
+        if (!more && qn == 0) break;
       }
       __syncthreads();
       // verification: every slot non-empty and <= tguess

@@ -37,6 +37,7 @@ struct WarpScratch {
   uint64_t next_off;    // absolute bit offset after the batch
   uint32_t epoch;       // Fisher-Yates map epoch (one per warp-processed element)
   uint32_t pad;
+  int32_t sq[64];       // survivor queue of the large-set path (element indices)
 };
 
 // Dense per-warp Fisher-Yates map with O(1) reset: entry = epoch << 16 | value
