@@ -127,6 +127,17 @@ int pmh_allpairs_tile(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0,
                       int64_t r1, int64_t c0, int64_t c1, uint16_t* out,
                       int64_t ld, void* stream);
 
+/*
+ * All-pairs reduction over rows [r0,r1) x cols [c0,c1) (pairs j > i): adds to
+ * hist[c] (uint64[m+1], caller-zeroed) the number of pairs with c equal
+ * components, and appends every pair with count >= thr to pairs as
+ * {(i << 32) | j, count} (uint64[2*cap]); *cursor (caller-zeroed uint64)
+ * ends at the number of such pairs (entries beyond cap are dropped).
+ */
+int pmh_allpairs_hist(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0, int64_t r1,
+                      int64_t c0, int64_t c1, int32_t thr, uint64_t* hist, uint64_t* pairs,
+                      int64_t cap, uint64_t* cursor, void* stream);
+
 /* b-bit reduction of nsets*m components (estimate.py:105-114, K:851-861). */
 int pmh_bbit(const uint64_t* sig, int64_t nsets, int64_t m, int b,
              int64_t* out, void* stream);

@@ -166,6 +166,31 @@ def allpairs_tile_device(sigs, r0, r1, c0, c1, out=None):
     return out
 
 
+def allpairs_hist_device(sigs, r0=0, r1=None, c0=0, c1=None, threshold=1, cap=1 << 22,
+                         hist=None):
+    """Histogram (int64 [m+1], CUDA) of equal-component counts over the pairs
+    (i, j), j > i, of rows [r0,r1) x cols [c0,c1), plus the pairs with count >=
+    threshold: returns (hist, pairs int64 [K, 3] numpy (i, j, count), total K)."""
+    torch = _torch()
+    n, m = sigs.shape
+    r1 = n if r1 is None else r1
+    c1 = n if c1 is None else c1
+    if hist is None:
+        hist = torch.zeros(m + 1, dtype=torch.int64, device=sigs.device)
+    pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=sigs.device)
+    cursor = torch.zeros(1, dtype=torch.int64, device=sigs.device)
+    rc = _lib.load().pmh_allpairs_hist(sigs.contiguous().data_ptr(), n, m, r0, r1, c0, c1,
+                                       int(threshold), hist.data_ptr(), pairs.data_ptr(), cap,
+                                       cursor.data_ptr(), _stream_ptr(torch, sigs.device))
+    _lib.check(rc)
+    k = int(cursor.item())
+    got = pairs[: min(k, cap)].cpu().numpy()
+    ij = got[:, 0].view(np.uint64)
+    out = np.stack([(ij >> np.uint64(32)).astype(np.int64),
+                    (ij & np.uint64(0xFFFFFFFF)).astype(np.int64), got[:, 1]], axis=1)
+    return hist, out, k
+
+
 def bbit_device(sig, b: int):
     torch = _torch()
     S, m = sig.shape

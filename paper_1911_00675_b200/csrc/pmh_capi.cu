@@ -603,6 +603,32 @@ int pmh_allpairs_tile(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0,
   return PMH_OK;
 }
 
+int pmh_allpairs_hist(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0, int64_t r1,
+                      int64_t c0, int64_t c1, int32_t thr, uint64_t* hist, uint64_t* pairs,
+                      int64_t cap, uint64_t* cursor, void* stream) {
+  if (m < 1 || m > 65535 || r0 < 0 || r1 > n || c0 < 0 || c1 > n || r0 > r1 || c0 > c1)
+    return set_error(PMH_ERR_INVALID, "bad tile bounds");
+  if (r0 == r1 || c0 == c1) return PMH_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = 2 * sizeof(uint64_t) * AP_KS * (AP_TILE + 1) + sizeof(unsigned) * (size_t)(m + 1);
+  PMH_CUDA(cudaFuncSetAttribute(allpairs_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, allpairs_hist_kernel, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ntiles = ((r1 - r0 + AP_TILE - 1) / AP_TILE) * ((c1 - c0 + AP_TILE - 1) / AP_TILE);
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > ntiles) grid = ntiles;
+  allpairs_hist_kernel<<<(unsigned)grid, 256, smem, st>>>(
+      sigs, m, r0, r1, c0, c1, thr, (unsigned long long*)hist, (unsigned long long*)pairs, cap,
+      (unsigned long long*)cursor);
+  PMH_CUDA(cudaGetLastError());
+  return PMH_OK;
+}
+
 int pmh_bbit(const uint64_t* sig, int64_t nsets, int64_t m, int b, int64_t* out,
              void* stream) {
   if (b < 1 || b > 16) return set_error(PMH_ERR_INVALID, "b must be in 1..16");

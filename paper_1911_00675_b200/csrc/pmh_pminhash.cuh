@@ -407,6 +407,81 @@ __global__ void __launch_bounds__(256) allpairs_tile_kernel(
   }
 }
 
+// All-pairs reduction (configs[4]): persistent CTAs walk the 64x64 pair
+// tiles of rows [r0,r1) x cols [c0,c1) (upper triangle j > i only), count
+// equal components exactly (64-bit compares of the staged signatures), and
+// reduce on the fly: a per-CTA shared histogram of the counts (flushed once
+// to `hist`, m+1 bins) and, for count >= thr, the pair appended to `pairs`
+// as (i << 32 | j, count) through a global cursor (dropped beyond `cap`; the
+// cursor still counts them).  No dense count matrix is materialised.
+__global__ void __launch_bounds__(256) allpairs_hist_kernel(
+    const uint64_t* __restrict__ sigs, int64_t m, int64_t r0, int64_t r1, int64_t c0,
+    int64_t c1, int32_t thr, unsigned long long* __restrict__ hist,
+    unsigned long long* __restrict__ pairs, int64_t cap, unsigned long long* __restrict__ cursor) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t (*sa)[AP_TILE + 1] = reinterpret_cast<uint64_t (*)[AP_TILE + 1]>(smem);
+  uint64_t (*sb)[AP_TILE + 1] =
+      reinterpret_cast<uint64_t (*)[AP_TILE + 1]>(smem + sizeof(uint64_t) * AP_KS * (AP_TILE + 1));
+  unsigned int* shist =
+      reinterpret_cast<unsigned int*>(smem + 2 * sizeof(uint64_t) * AP_KS * (AP_TILE + 1));
+  for (int64_t b = threadIdx.x; b <= m; b += blockDim.x) shist[b] = 0;
+  __syncthreads();
+  const int64_t nti = (r1 - r0 + AP_TILE - 1) / AP_TILE, ntj = (c1 - c0 + AP_TILE - 1) / AP_TILE;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  for (int64_t t = blockIdx.x; t < nti * ntj; t += gridDim.x) {
+    const int64_t ti = r0 + (t / ntj) * AP_TILE, tj = c0 + (t % ntj) * AP_TILE;
+    if (tj + AP_TILE <= ti + 1) continue;  // entirely on/below the diagonal
+    int cnt[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+#pragma unroll
+      for (int v = 0; v < 4; v++) cnt[u][v] = 0;
+    for (int64_t k0 = 0; k0 < m; k0 += AP_KS) {
+      __syncthreads();
+      for (int q = threadIdx.x; q < AP_KS * AP_TILE; q += blockDim.x) {
+        const int r = q / AP_KS, kk = q % AP_KS;
+        const int64_t gi = ti + r, gj = tj + r, k = k0 + kk;
+        sa[kk][r] = (gi < r1 && k < m) ? __ldg(&sigs[gi * m + k]) : 0x1ULL;
+        sb[kk][r] = (gj < c1 && k < m) ? __ldg(&sigs[gj * m + k]) : 0x2ULL;
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int kk = 0; kk < AP_KS; kk++) {
+        uint64_t av[4], bv[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) av[u] = sa[kk][ty * 4 + u];
+#pragma unroll
+        for (int v = 0; v < 4; v++) bv[v] = sb[kk][tx * 4 + v];
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+          for (int v = 0; v < 4; v++) cnt[u][v] += (av[u] == bv[v]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int64_t i = ti + ty * 4 + u;
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        const int64_t j = tj + tx * 4 + v;
+        if (i < r1 && j < c1 && j > i) {
+          atomicAdd(&shist[cnt[u][v]], 1u);
+          if (cnt[u][v] >= thr) {
+            const unsigned long long pos = atomicAdd(cursor, 1ULL);
+            if ((int64_t)pos < cap) {
+              pairs[2 * pos] = ((unsigned long long)i << 32) | (unsigned long long)j;
+              pairs[2 * pos + 1] = (unsigned long long)cnt[u][v];
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int64_t b = threadIdx.x; b <= m; b += blockDim.x)
+    if (shist[b]) atomicAdd(&hist[b], (unsigned long long)shist[b]);
+}
+
 // b-bit reduction (K:851-861): component i -> low b bits of
 // mix64(sig_i + GOLDEN*(i+1)); one thread per component of a [nsets, m] batch
 __global__ void bbit_kernel(const uint64_t* __restrict__ sig, int64_t total,

@@ -140,6 +140,21 @@ def _gpu_count_tile(sigs_all, r0, r1, c0, c1):
     return out.cpu().numpy().view(np.uint16)
 
 
+def _gpu_rows_hist(sigs_all, rows, tile, threshold):
+    """This rank's block rows on the GPU with the fused histogram kernel."""
+    import torch
+    from .batch import allpairs_hist_device
+    n, m = sigs_all.shape
+    hist = torch.zeros(m + 1, dtype=torch.int64, device=sigs_all.device)
+    found = []
+    for b in rows:
+        r0, r1 = b * tile, min(n, (b + 1) * tile)
+        _, pairs, k = allpairs_hist_device(sigs_all, r0, r1, r0, n, threshold, hist=hist)
+        found.append(pairs)
+    pairs = np.concatenate(found) if found else np.zeros((0, 3), np.int64)
+    return AllPairsResult(hist.cpu().numpy(), pairs, len(rows))
+
+
 def allpairs_distributed(local_sigs, rank, world, tile=4096, threshold=1, group=None,
                          count_tile_fn=None):
     """All-gather the sharded signatures, compute this rank's block rows and
@@ -161,8 +176,10 @@ def allpairs_distributed(local_sigs, rank, world, tile=4096, threshold=1, group=
     sigs_all = torch.cat([g[:s] for g, s in zip(gathered, sizes)], dim=0)
     n = sigs_all.shape[0]
     rows = block_rows(n, tile, world)[rank]
-    fn = count_tile_fn or _gpu_count_tile
-    res = allpairs_local(sigs_all, rows, tile, threshold, fn)
+    if count_tile_fn is None:
+        res = _gpu_rows_hist(sigs_all, rows, tile, threshold)
+    else:
+        res = allpairs_local(sigs_all, rows, tile, threshold, count_tile_fn)
     h = torch.from_numpy(res.hist).to(local_sigs.device)
     dist.all_reduce(h, group=group)
     res.hist = h.cpu().numpy()
