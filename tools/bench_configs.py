@@ -1,0 +1,104 @@
+"""Secondary measurements for BASELINE.json configs[0], [2], [3], [4] on one
+GPU (bench.py measures the headline configs[1]).  Device-resident inputs,
+CUDA-event timing (1 warm-up + 3 timed runs, min and mean reported), one JSON
+line per measurement.  Elements/s counts every element of the batch once per
+variant; all-pairs reports pairs/s and equal-component compares/s."""
+import argparse
+import ctypes
+import json
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_1911_00675_b200 import _lib, datagen  # noqa: E402
+from paper_1911_00675_b200.batch import (allpairs_hist_device, to_device_f64,  # noqa: E402
+                                         to_device_i64, to_device_u64)
+
+L = _lib.load()
+
+
+def timed(fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return min(ts), float(np.mean(ts))
+
+
+def sketch_fn(algo, m, ids, w, off, S, sig, status):
+    sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def f():
+        _lib.check(L.pmh_sketch_csr_async(_lib.ALG[algo], m, ids.data_ptr(),
+                                          w.data_ptr() if w is not None else None, off.data_ptr(),
+                                          S, sig.data_ptr(), None, status.data_ptr(), sp))
+    return f
+
+
+def run_sketch(cfg, batch, algos, m):
+    ids = to_device_u64(batch.ids)
+    w = to_device_f64(batch.weights) if batch.weights is not None else None
+    off = to_device_i64(batch.offsets)
+    S, N = batch.nsets, batch.nelems
+    sig = torch.empty((S, m), dtype=torch.int64, device="cuda")
+    status = torch.empty(2, dtype=torch.int64, device="cuda")
+    out = {}
+    for a in algos:
+        _lib.check(L.pmh_status_reset(status.data_ptr(), None))
+        tmin, tmean = timed(sketch_fn(a, m, ids, w, off, S, sig, status))
+        err = ctypes.c_int64(-1)
+        _lib.check(L.pmh_status_check(status.data_ptr(), ctypes.byref(err), None), err.value)
+        line = {"config": cfg, "algo": a, "m": m, "sets": S, "elements": N,
+                "ms_min": tmin, "ms_mean": tmean, "elements_per_s": N / (tmin / 1e3)}
+        print(json.dumps(line), flush=True)
+        out[a] = sig.clone() if a == algos[-1] else None
+    return sig
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,3,4,5")
+    args = ap.parse_args()
+    cfgs = args.configs.split(",")
+    if "1" in cfgs:
+        run_sketch("configs[0] PMH3 m=256 1000x1000", datagen.config1(), ["probminhash3",
+                                                                          "probminhash3a"], 256)
+    if "3" in cfgs:
+        b = datagen.config3()
+        run_sketch("configs[2] unweighted m=4096 100000x1000", b,
+                   ["unweighted1", "unweighted1a", "unweighted2", "unweighted3", "unweighted3a",
+                    "unweighted4"], 4096)
+        del b
+    if "4" in cfgs:
+        run_sketch("configs[3] PMH2/PMH4 (non-streaming == streaming) m=64 1e6x100 Pareto1.5",
+                   datagen.config4(), ["probminhash2", "probminhash4"], 64)
+    if "5" in cfgs:
+        b, jt, jx = datagen.config5_pairs()
+        sig = run_sketch("configs[4] PMH4 m=256 100000x500 (50k pairs)", b, ["probminhash4"], 256)
+        n = sig.shape[0]
+        box = {}
+
+        def ap_fn():
+            box["r"] = allpairs_hist_device(sig, threshold=1, cap=1 << 20)
+        tmin, tmean = timed(ap_fn, reps=2)
+        hist, pairs, k = box["r"]
+        npairs = n * (n - 1) // 2
+        print(json.dumps({"config": "configs[4] all-pairs equal-component counts", "n": n,
+                          "m": 256, "pairs": npairs, "ms_min": tmin, "ms_mean": tmean,
+                          "pairs_per_s": npairs / (tmin / 1e3),
+                          "compares_per_s": npairs * 256 / (tmin / 1e3),
+                          "pairs_with_count_ge_1": k}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
