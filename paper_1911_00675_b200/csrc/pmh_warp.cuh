@@ -38,6 +38,7 @@ struct WarpScratch {
   uint32_t epoch;       // Fisher-Yates map epoch (one per warp-processed element)
   uint32_t pad;
   int32_t sq[64];       // survivor queue of the large-set path (element indices)
+  uint32_t gm[32];      // parallel Fisher-Yates: lanes whose target is i0 + k
 };
 
 // Dense per-warp Fisher-Yates map with O(1) reset: entry = epoch << 16 | value
@@ -322,6 +323,49 @@ __device__ __forceinline__ void fy_steps(WarpScratch& ws, EpochFY fy, int64_t i0
   }
 }
 
+// Warp-parallel lazy Fisher-Yates for the q points of a batch (lane k =
+// point pt_k = i0 + k with index j_k = pt_k + r_k, K:222-235).  Sequentially:
+//   out_k = P[j_k];  P[j_k] = P[pt_k]
+// so with v_k = P_{k-1}[pt_k]: v_k is the v of the latest earlier lane whose
+// target j equals pt_k (else the map before the batch), out_k is the v of the
+// latest earlier lane with the same target j_k (else the map before the batch),
+// and each distinct target finally holds the v of its last writer.  Earlier
+// writers come from __match_any_sync; the (short) v chains resolve by shuffle
+// pointer chasing.
+__device__ __forceinline__ void fy_steps_parallel(WarpScratch& ws, EpochFY fy, int64_t i0,
+                                                  uint32_t q, int lane) {
+  const bool valid = (uint32_t)lane < q;
+  const int32_t pt = (int32_t)(i0 + lane);
+  const int32_t j = valid ? pt + ws.lab[lane] : -1 - lane;
+  ws.gm[lane] = 0u;
+  __syncwarp();
+  const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+  unsigned grp = 0u;
+  if (valid) grp = __match_any_sync(vmask, j);
+  const int last = valid ? 31 - __clz((int)grp) : -1;   // last writer of target j
+  if (valid && lane == last && j - (int32_t)i0 < 32) ws.gm[j - (int32_t)i0] = grp;
+  const int32_t pb_pt = valid ? fy.get(pt) : 0;         // map before the batch
+  const int32_t pb_j = valid ? fy.get(j) : 0;
+  __syncwarp();
+  const unsigned below = (1u << lane) - 1u;
+  const unsigned pm = valid ? (ws.gm[lane] & below) : 0u;
+  const int prevp = pm ? 31 - __clz((int)pm) : lane;
+  const unsigned jm = grp & below;
+  const int prevj = jm ? 31 - __clz((int)jm) : lane;
+  int32_t v = pb_pt;
+  bool pend = valid && prevp != lane;
+  while (__any_sync(0xffffffffu, pend)) {
+    const int32_t vs = __shfl_sync(0xffffffffu, v, prevp);
+    const bool ps = __shfl_sync(0xffffffffu, pend, prevp);
+    if (pend && !ps) { v = vs; pend = false; }
+  }
+  const int32_t vj = __shfl_sync(0xffffffffu, v, prevj);
+  __syncwarp();
+  if (valid && lane == last) fy.set(j, v);
+  if (valid) ws.lab[lane] = prevj != lane ? vj : pb_j;
+  __syncwarp();
+}
+
 template <int F>
 __device__ int warp_el_fy(SetCtx& c, const Tables& T, WarpScratch& ws, uint32_t* fy, int lane,
                           int64_t e, uint64_t id, double winv) {
@@ -375,8 +419,7 @@ __device__ int warp_el_fy(SetCtx& c, const Tables& T, WarpScratch& ws, uint32_t*
     } else if constexpr (F == FAM_UW4) {
       tv = (double)u * INV53;  // the uniform itself
     }
-    if (lane == 0) fy_steps(ws, efy, i, q);
-    __syncwarp();
+    fy_steps_parallel(ws, efy, i, q, lane);
     const double thr = warp_thr(c);
     const bool in = (uint32_t)lane < q;
     double xv = 0.0;
