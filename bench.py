@@ -72,12 +72,24 @@ class ClockSampler:
         self.samples = []
         self._stop = threading.Event()
         self._t = None
-
-    def _run(self):
+        # NVML init + a first query happen HERE, outside the timed region (a
+        # first NVML call takes driver locks that would stall kernel enqueues)
+        self._nvml = None
         try:
             import pynvml
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            self._nvml = (pynvml, h)
+        except Exception:
+            self._nvml = None
+
+    def _run(self):
+        try:
+            if self._nvml is None:
+                raise RuntimeError("no nvml")
+            pynvml, h = self._nvml
             bits = [pynvml.nvmlClocksThrottleReasonHwSlowdown,
                     pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
                     pynvml.nvmlClocksThrottleReasonSwThermalSlowdown,
@@ -245,10 +257,11 @@ def main():
     torch.cuda.synchronize()
 
     ev = {v: [] for v in variants}
+    clk_sampler = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with clk_sampler as clk:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)

@@ -360,7 +360,7 @@ int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
   const bool pmin = algo == ALG_PMINHASH || algo == ALG_MINHASH;
   OrderWs ow;
   // cost offset: ProbMinHash families pay ~m ln m points per set regardless of n
-  e = build_order(offsets, nsets, pmin ? 0 : (int64_t)(7.0 * (double)m), pmin ? -1 : SMALL_N,
+  e = build_order(offsets, nsets, pmin ? 0 : (int64_t)(7.0 * (double)m), pmin ? -1 : small_n_for(m),
                   4096, st, &ow);
   if (e != cudaSuccess) return cuda_fail(e, "set ordering");
   int32_t* order = ow.order;

@@ -51,6 +51,119 @@ __host__ __device__ inline size_t sketch_smem_bytes(int family, int64_t m, int t
   return (b + 15) & ~(size_t)15;
 }
 
+// Per-warp element loop shared by the CTA-per-set and warp-per-set kernels:
+// chunks of up to 32 elements come from `grab` (a shared counter or a private
+// cursor); the next chunk's ids/weights are loaded before the current one is
+// processed (global-load latency overlaps the work).  Every element first runs
+// the division-free first-point prefilter; SURVIVORS are compacted into a
+// per-warp queue and run through the full recurrence 32 at a time, so the
+// expensive path executes with full warps instead of the few lanes that
+// survive in any one chunk (large sets keep only ~1-15%); elements expected
+// to be long (or whose Fisher-Yates state outgrows the lane map) run
+// warp-cooperatively.
+struct SharedGrab {
+  unsigned* ctr;
+  unsigned chunk;
+  __device__ __forceinline__ unsigned next(int lane) {
+    unsigned b = 0;
+    if (lane == 0) b = atomicAdd(ctr, chunk);
+    return __shfl_sync(0xffffffffu, b, 0);
+  }
+};
+struct LocalGrab {
+  unsigned cur;
+  unsigned chunk;
+  __device__ __forceinline__ unsigned next(int) { const unsigned b = cur; cur += chunk; return b; }
+};
+
+template <int F, class Grab>
+__device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const uint64_t* ids,
+                                           const double* w, int64_t n, int64_t chunk, Grab& grab,
+                                           WarpScratch* wscr, uint32_t* fy_dense, bool warp_ok,
+                                           bool& failed, int lane) {
+  unsigned base = grab.next(lane);
+  uint64_t id_nx = 0;
+  double w_nx = 1.0;
+  {
+    const int64_t e = (int64_t)base + lane;
+    if (lane < chunk && e < n) {
+      id_nx = __ldg(&ids[e]);
+      if (family_weighted(F) && w) w_nx = __ldg(&w[e]);
+    }
+  }
+  int since_refresh = 0;
+  int qn = 0;                                  // queued survivors (warp-uniform)
+  for (;;) {
+    const bool more = (int64_t)base < n;
+    if (more) {
+      const int64_t e = (int64_t)base + lane;
+      const bool active = lane < chunk && e < n;
+      const uint64_t id = id_nx;
+      const double wv = w_nx;
+      const unsigned nbase = grab.next(lane);
+      const int64_t en = (int64_t)nbase + lane;
+      if (lane < chunk && en < n) {
+        id_nx = __ldg(&ids[en]);
+        if (family_weighted(F) && w) w_nx = __ldg(&w[en]);
+      }
+      bool surv = false;
+      if (active) {
+        surv = !first_point_rejects<F>(c, T, id, wv, ctx_thr(c));
+        if (!surv) c.points += (0.0 > c.tprev);          // rejected first point
+      }
+      const unsigned sm = __ballot_sync(0xffffffffu, surv);
+      if (surv) wscr->sq[qn + __popc(sm & ((1u << lane) - 1u))] = (int32_t)e;
+      qn += __popc(sm);
+      base = nbase;
+      __syncwarp();
+    }
+    if (qn >= 32 || (!more && qn > 0)) {
+      // run up to 32 queued survivors, one per lane
+      const int take = qn < 32 ? qn : 32;
+      const bool act = lane < take;
+      const int64_t e = act ? (int64_t)wscr->sq[lane] : 0;
+      __syncwarp();
+      if (qn > 32 && lane < qn - 32) wscr->sq[lane] = wscr->sq[lane + 32];
+      qn -= take;
+      __syncwarp();
+      const int64_t upd0 = c.updates;
+      uint64_t id = 0;
+      double winv = 1.0;
+      bool heavy = false;
+      int status = EL_DONE;
+      if (act) {
+        id = __ldg(&ids[e]);
+        if (family_weighted(F) && w) winv = 1.0 / __ldg(&w[e]);
+        heavy = warp_ok && ctx_thr(c) > HEAVY_POINTS * winv;
+        if (!heavy) {
+          SparseFY fy; fy.reset();
+          status = run_element<F>(c, T, fy, e, id, winv);
+        }
+      }
+      if (status == EL_FAIL) failed = true;
+      unsigned hm = __ballot_sync(0xffffffffu, act && (heavy || status == EL_NEED_WARP));
+      while (hm) {
+        const int l = __ffs(hm) - 1;
+        hm &= hm - 1;
+        const int64_t eh = __shfl_sync(0xffffffffu, e, l);
+        const uint64_t idh = __shfl_sync(0xffffffffu, id, l);
+        const double winvh = __shfl_sync(0xffffffffu, winv, l);
+        const int st = warp_element<F>(c, T, *wscr, fy_dense, lane, eh, idh, winvh);
+        if (st == EL_FAIL) failed = true;
+        if (lane == 0) c.multi++;
+        __syncwarp();
+      }
+      // refresh h_max after batches that lowered a slot (and every 8th)
+      const bool changed = __any_sync(0xffffffffu, c.updates != upd0);
+      if (changed || ++since_refresh >= 8) {
+        hmax_refresh_warp(c, lane);
+        since_refresh = 0;
+      }
+    }
+    if (!more && qn == 0) break;
+  }
+}
+
 // Dynamic shared memory: Slot[m] | WarpScratch[nwarps] | int32 FY[nwarps][m+1]
 #ifndef SKETCH_MINBLOCKS
 #define SKETCH_MINBLOCKS 2
@@ -136,98 +249,8 @@ __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS) sketch_sets_
       c.tguess = tg;
       if (threadIdx.x == 0) s_next = 0;
       __syncthreads();
-      // Chunks of 32 elements are pulled from a shared counter; the next
-      // chunk's ids/weights are loaded before the current one is processed
-      // (global-load latency overlaps the work).  Every element first runs the
-      // division-free first-point prefilter; SURVIVORS are compacted into a
-      // per-warp queue and run through the full recurrence 32 at a time, so
-      // the expensive path executes with full warps instead of the few lanes
-      // that survive in any one chunk (large sets keep only ~1-15%).
-      unsigned base = 0;
-      if (lane == 0) base = atomicAdd(&s_next, (unsigned)chunk);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      uint64_t id_nx = 0;
-      double w_nx = 1.0;
-      {
-        const int64_t e = (int64_t)base + lane;
-        if (lane < chunk && e < n) {
-          id_nx = __ldg(&ids[e]);
-          if (family_weighted(F) && w) w_nx = __ldg(&w[e]);
-        }
-      }
-      int since_refresh = 0;
-      int qn = 0;                                  // queued survivors (warp-uniform)
-      for (;;) {
-        const bool more = (int64_t)base < n;
-        if (more) {
-          const int64_t e = (int64_t)base + lane;
-          const bool active = lane < chunk && e < n;
-          const uint64_t id = id_nx;
-          const double wv = w_nx;
-          unsigned nbase = 0;
-          if (lane == 0) nbase = atomicAdd(&s_next, (unsigned)chunk);
-          nbase = __shfl_sync(0xffffffffu, nbase, 0);
-          const int64_t en = (int64_t)nbase + lane;
-          if (lane < chunk && en < n) {
-            id_nx = __ldg(&ids[en]);
-            if (family_weighted(F) && w) w_nx = __ldg(&w[en]);
-          }
-          bool surv = false;
-          if (active) {
-            surv = !first_point_rejects<F>(c, a.T, id, wv, ctx_thr(c));
-            if (!surv) c.points += (0.0 > c.tprev);          // rejected first point
-          }
-          const unsigned sm = __ballot_sync(0xffffffffu, surv);
-          if (surv) wscr->sq[qn + __popc(sm & ((1u << lane) - 1u))] = (int32_t)e;
-          qn += __popc(sm);
-          base = nbase;
-          __syncwarp();
-        }
-        if (qn >= 32 || (!more && qn > 0)) {
-          // run up to 32 queued survivors, one per lane
-          const int take = qn < 32 ? qn : 32;
-          const bool act = lane < take;
-          const int64_t e = act ? (int64_t)wscr->sq[lane] : 0;
-          __syncwarp();
-          if (qn > 32 && lane < qn - 32) wscr->sq[lane] = wscr->sq[lane + 32];
-          qn -= take;
-          __syncwarp();
-          const int64_t upd0 = c.updates;
-          uint64_t id = 0;
-          double winv = 1.0;
-          bool heavy = false;
-          int status = EL_DONE;
-          if (act) {
-            id = __ldg(&ids[e]);
-            if (family_weighted(F) && w) winv = 1.0 / __ldg(&w[e]);
-            heavy = warp_ok && ctx_thr(c) > HEAVY_POINTS * winv;
-            if (!heavy) {
-              SparseFY fy; fy.reset();
-              status = run_element<F>(c, a.T, fy, e, id, winv);
-            }
-          }
-          if (status == EL_FAIL) failed = true;
-          unsigned hm = __ballot_sync(0xffffffffu, act && (heavy || status == EL_NEED_WARP));
-          while (hm) {
-            const int l = __ffs(hm) - 1;
-            hm &= hm - 1;
-            const int64_t eh = __shfl_sync(0xffffffffu, e, l);
-            const uint64_t idh = __shfl_sync(0xffffffffu, id, l);
-            const double winvh = __shfl_sync(0xffffffffu, winv, l);
-            const int st = warp_element<F>(c, a.T, *wscr, fy_dense, lane, eh, idh, winvh);
-            if (st == EL_FAIL) failed = true;
-            if (lane == 0) c.multi++;
-            __syncwarp();
-          }
-          // refresh h_max after batches that lowered a slot (and every 8th)
-          const bool changed = __any_sync(0xffffffffu, c.updates != upd0);
-          if (changed || ++since_refresh >= 8) {
-            hmax_refresh_warp(c, lane);
-            since_refresh = 0;
-          }
-        }
-        if (!more && qn == 0) break;
-      }
+      SharedGrab grab{&s_next, (unsigned)chunk};
+      warp_elements<F>(c, a.T, ids, w, n, chunk, grab, wscr, fy_dense, warp_ok, failed, lane);
       __syncthreads();
       // verification: every slot non-empty and <= tguess
       unsigned long long mx = 0;
@@ -279,13 +302,26 @@ __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS) sketch_sets_
 namespace pmh {
 
 // ---------------------------------------------------------------------------
-// Small sets (n <= SMALL_N): one WARP per set.  Their cost is the coupon-
-// collector phase (~m (ln m + c) points, all in long per-element sequences),
-// so every element runs warp-cooperatively (mode B) and a CTA-per-set layout
-// would idle 7 of 8 warps.  Each warp owns a private slot table, scratch and
-// Fisher-Yates map in shared memory.
+// Small sets (n <= small_n(m)): one WARP per set, with a private slot table,
+// scratch and Fisher-Yates map in shared memory, running the same element
+// loop as the CTA kernel (warp_elements) over a private cursor.  For m = 1024
+// this is the tiny sets (n <= 3: their coupon-collector phase keeps one warp
+// busy and a CTA-per-set layout would idle 7 of 8 warps); for small m
+// (configs[3]: m = 64, n = 100) whole sets are cheap and the CTA kernel's
+// per-set barriers dominate, so they all run warp-per-set.
 // ---------------------------------------------------------------------------
-constexpr int64_t SMALL_N = 3;   // measured: warp-per-set wins only below ~4 elements
+#ifndef PMH_SMALL_N
+#define PMH_SMALL_N 3
+#endif
+constexpr int64_t SMALL_N = PMH_SMALL_N;   // sets up to this size run warp-per-set (measured)
+#ifndef PMH_SMALL_N_SMALLM
+#define PMH_SMALL_N_SMALLM 512
+#endif
+// warp-per-set cutoff: for m <= 256 whole sets of up to 512 elements are cheap
+// enough for one warp (configs[3], configs[4]); for large m only tiny sets
+__host__ __device__ inline int64_t small_n_for(int64_t m) {
+  return m <= 256 ? (int64_t)PMH_SMALL_N_SMALLM : SMALL_N;
+}
 
 struct WarpSetVars {
   unsigned long long hmax;
@@ -351,25 +387,8 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
     bool failed = false;
     for (int attempt = 0;; attempt++) {
       c.tguess = tg;
-      for (int64_t e = 0; e < n && !failed; e++) {
-        const uint64_t id = ids[e];
-        const double winv = (family_weighted(F) && w) ? 1.0 / w[e] : 1.0;
-        int st;
-        if (warp_ok) {
-          st = warp_element<F>(c, a.T, *ws, fy, lane, e, id, winv);
-        } else {
-          st = EL_DONE;
-          if (lane == 0) {
-            SparseFY sfy; sfy.reset();
-            st = run_element<F>(c, a.T, sfy, e, id, winv);
-            if (st == EL_DONE) hmax_recompute_serial(c);
-          }
-          st = __shfl_sync(0xffffffffu, st, 0);
-        }
-        if (st == EL_FAIL) failed = true;
-        if (lane == 0) c.multi++;
-        __syncwarp();
-      }
+      LocalGrab grab{0u, 32u};
+      warp_elements<F>(c, a.T, ids, w, n, 32, grab, ws, fy, warp_ok, failed, lane);
       unsigned long long mx = 0;
       for (int64_t k = lane; k < m; k += 32) {
         const unsigned long long h = slots[k].h;
@@ -393,14 +412,15 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
       sig[k] = ix < (unsigned long long)n ? ids[ix] : 0ULL;
     }
     if (a.stats) {
-      long long pts = c.points, upd = c.updates;
+      long long pts = c.points, upd = c.updates, mul = c.multi;
       for (int o = 16; o > 0; o >>= 1) {
         pts += __shfl_xor_sync(0xffffffffu, pts, o);
         upd += __shfl_xor_sync(0xffffffffu, upd, o);
+        mul += __shfl_xor_sync(0xffffffffu, mul, o);
       }
       if (lane == 0) {
         a.stats[s * 3 + 0] = pts;
-        a.stats[s * 3 + 1] = c.multi;
+        a.stats[s * 3 + 1] = mul;
         a.stats[s * 3 + 2] = upd;
       }
     }
