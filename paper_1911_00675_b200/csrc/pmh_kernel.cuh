@@ -166,7 +166,7 @@ __device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const 
 
 // Dynamic shared memory: Slot[m] | WarpScratch[nwarps] | int32 FY[nwarps][m+1]
 #ifndef SKETCH_MINBLOCKS
-#define SKETCH_MINBLOCKS 2
+#define SKETCH_MINBLOCKS 3   // 80 registers, 3 CTAs/SM: measured 3-12% faster than 2
 #endif
 template <int F>
 __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS) sketch_sets_kernel(SketchArgs a) {
