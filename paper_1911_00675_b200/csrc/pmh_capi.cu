@@ -514,6 +514,10 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
     while (lo < hi) { const int64_t mid = (lo + hi) / 2; if (offsets[mid] < target) lo = mid + 1; else hi = mid; }
     cut[c] = lo;
   }
+  // each chunk of the first algorithm runs on its own stream so the chunks'
+  // LPT tails overlap (one stream would serialise four tails)
+  cudaStream_t cst[4] = {nullptr, nullptr, nullptr, nullptr};
+  for (int c = 0; c < NC; c++) cudaStreamCreateWithFlags(&cst[c], cudaStreamNonBlocking);
   for (int c = 0; c < NC && rc == PMH_OK; c++) {
     const int64_t e0 = offsets[cut[c]], e1 = offsets[cut[c + 1]];
     if (e1 > e0) {
@@ -527,14 +531,17 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
     }
     cudaEvent_t ev = mkev();
     cudaEventRecord(ev, cin);
-    cudaStreamWaitEvent(st, ev, 0);
+    cudaStreamWaitEvent(cst[c], ev, 0);
     const int64_t ns = cut[c + 1] - cut[c];
     if (ns > 0) {
       uint64_t* sig0 = (uint64_t*)d_out + (size_t)cut[c] * m;
       int64_t* st0 = want_stats ? (int64_t*)(d_out + bs) + 3 * cut[c] : nullptr;
       rc = pmh_sketch_csr_async(algos[0], m, d_ids, weighted ? d_w : nullptr, d_off + cut[c], ns,
-                                sig0, st0, d_status, st);
+                                sig0, st0, d_status, cst[c]);
     }
+    cudaEvent_t evc = mkev();
+    cudaEventRecord(evc, cst[c]);
+    cudaStreamWaitEvent(st, evc, 0);
   }
   // remaining algorithms over the whole batch; each result's D2H overlaps the
   // next algorithm's compute on the copy-out stream
@@ -562,6 +569,7 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
   cudaFreeAsync(d, st);
   e = cudaStreamSynchronize(st);
   for (auto ev : evs) cudaEventDestroy(ev);
+  for (int c = 0; c < NC; c++) if (cst[c]) cudaStreamDestroy(cst[c]);
   cudaStreamDestroy(st); cudaStreamDestroy(cin); cudaStreamDestroy(cout);
   if (rc == PMH_OK && e != cudaSuccess) rc = cuda_fail(e, "sync");
   return rc;
