@@ -117,22 +117,24 @@ __device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const 
       base = nbase;
       __syncwarp();
     }
+    const int64_t upd0 = c.updates;
+    bool ran = false;
+    unsigned hm = 0;                             // lanes whose element runs warp-wide
+    int64_t e = 0;
     if (qn >= 32 || (!more && qn > 0)) {
       // run up to 32 queued survivors, one per lane
       const int take = qn < 32 ? qn : 32;
       const bool act = lane < take;
-      const int64_t e = act ? (int64_t)wscr->sq[lane] : 0;
+      e = act ? (int64_t)wscr->sq[lane] : 0;
       __syncwarp();
       if (qn > 32 && lane < qn - 32) wscr->sq[lane] = wscr->sq[lane + 32];
       qn -= take;
       __syncwarp();
-      const int64_t upd0 = c.updates;
-      uint64_t id = 0;
-      double winv = 1.0;
       bool heavy = false;
       int status = EL_DONE;
       if (act) {
-        id = __ldg(&ids[e]);
+        const uint64_t id = __ldg(&ids[e]);
+        double winv = 1.0;
         if (family_weighted(F) && w) winv = 1.0 / __ldg(&w[e]);
         heavy = warp_ok && ctx_thr(c) > HEAVY_POINTS * winv;
         if (!heavy) {
@@ -141,18 +143,24 @@ __device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const 
         }
       }
       if (status == EL_FAIL) failed = true;
-      unsigned hm = __ballot_sync(0xffffffffu, act && (heavy || status == EL_NEED_WARP));
-      while (hm) {
-        const int l = __ffs(hm) - 1;
-        hm &= hm - 1;
-        const int64_t eh = __shfl_sync(0xffffffffu, e, l);
-        const uint64_t idh = __shfl_sync(0xffffffffu, id, l);
-        const double winvh = __shfl_sync(0xffffffffu, winv, l);
-        const int st = warp_element<F>(c, T, *wscr, fy_dense, lane, eh, idh, winvh);
-        if (st == EL_FAIL) failed = true;
-        if (lane == 0) c.multi++;
-        __syncwarp();
-      }
+      const bool want = act && (heavy || status == EL_NEED_WARP);
+      hm = __ballot_sync(0xffffffffu, want);
+      ran = true;
+    }
+    // warp-cooperative elements of this batch, one at a time
+    while (hm) {
+      const int l = __ffs(hm) - 1;
+      hm &= hm - 1;
+      const int64_t eh = __shfl_sync(0xffffffffu, e, l);
+      const uint64_t idh = __ldg(&ids[eh]);
+      const double winvh = (family_weighted(F) && w) ? 1.0 / __ldg(&w[eh]) : 1.0;
+      const int st = warp_element<F>(c, T, *wscr, fy_dense, lane, eh, idh, winvh);
+      if (st == EL_FAIL) failed = true;
+      if (lane == 0) c.multi++;
+      __syncwarp();
+      ran = true;
+    }
+    if (ran) {
       // refresh h_max after batches that lowered a slot (and every 8th)
       const bool changed = __any_sync(0xffffffffu, c.updates != upd0);
       if (changed || ++since_refresh >= 8) {

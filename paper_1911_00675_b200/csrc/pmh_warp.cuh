@@ -28,7 +28,6 @@ constexpr uint32_t WIN_BITS = 2048;  // 32 words
 
 struct WarpScratch {
   uint64_t words[65];   // window (64 words for the parallel FY parse, +1 guard)
-  uint32_t acc[32];     // per-point label-acceptance masks (parallel FY parse)
   uint32_t eoff[32];    // window-relative bit offset of each point's first draw
   int32_t lab[32];      // 1-based labels
   double tval[32];      // TruncExp values (PMH4 parse), NaN => exponential draw
@@ -242,12 +241,31 @@ __device__ void parse_fy_cursor(const SetCtx& c, WarpScratch& ws, uint64_t id, u
   ws.next_off = (flags & 1u) ? next_off : (wb << 6) + cur;
 }
 
+// Bit t (t0 <= t < t1) set iff label round t (the kb-bit field at pos + kb t)
+// is accepted (< R).  Rounds are contiguous fields, so one 64-bit funnel load
+// serves fpw = 64 / kb of them.
+constexpr uint32_t ACC_ROUNDS0 = 8;
+__device__ __forceinline__ uint32_t accept_mask(const uint64_t* w, uint32_t pos, uint32_t kb,
+                                                uint64_t R, uint32_t t0, uint32_t t1,
+                                                uint32_t fpw) {
+  const uint64_t mask = (1ULL << kb) - 1ULL;
+  uint32_t acc = 0;
+  for (uint32_t t = t0; t < t1;) {
+    const uint32_t p = pos + kb * t, i = p >> 6, sh = p & 63;
+    const uint64_t win = sh ? (w[i] >> sh) | (w[i + 1] << (64 - sh)) : w[i];
+    const uint32_t te = t + fpw < t1 ? t + fpw : t1;
+    uint32_t fo = 0;
+    for (; t < te; t++, fo += kb) acc |= (((win >> fo) & mask) < R ? 1u : 0u) << t;
+  }
+  return acc;
+}
+
 // Warp-parallel version of parse_fy_cursor.  For a run of points whose
 // Fisher-Yates range R = m - pt + 1 shares the label width kb, point k starts
 // at base_k + kb * Y_k, where base_k = rel0 + k (53 + kb) and Y_k is the number
 // of REJECTED label rounds of points 0..k-1.  Lane k records in a 24-bit mask
 // which of its candidate label draws (base_k + 53 + kb t, t = 0..23) would be
-// accepted (< R_k); a warp-uniform scan Y_{k+1} = Y_k + ctz(acc_k >> Y_k) then
+// accepted (< R_k); the recurrence Y_{k+1} = Y_k + ctz(acc_k >> Y_k) then
 // fixes every offset (K:97-117 rejection semantics exactly).  Falls back to the
 // serial parse when the run is empty or a point rejects beyond the window.
 __device__ void parse_fy_parallel(const SetCtx& c, WarpScratch& ws, uint64_t id, uint64_t off,
@@ -275,25 +293,34 @@ __device__ void parse_fy_parallel(const SetCtx& c, WarpScratch& ws, uint64_t id,
   const unsigned runmask = __ballot_sync(0xffffffffu, inrun);
   const uint32_t qmax = runmask == 0xffffffffu ? 32u : (uint32_t)(__ffs(~runmask) - 1);
   const uint32_t base = rel0 + (uint32_t)lane * (53u + kb);
-  if ((uint32_t)lane < qmax) {
-    uint32_t acc = 0;
-#pragma unroll 4
-    for (uint32_t t = 0; t < 24; t++) {
-      const uint32_t pos = base + 53u + kb * t;
-      const uint64_t v = win_bits(ws.words, pos, kb);
-      acc |= (v < (uint64_t)R ? 1u : 0u) << t;
+  // rounds [0, 8) first: rejections are rare for most ranges, so the later
+  // rounds are only decoded when the scan runs past them
+  const uint32_t fpw = 64u / kb;   // label fields per 64-bit window load
+  const bool mine = (uint32_t)lane < qmax;
+  uint32_t acc = mine ? accept_mask(ws.words, base + 53u, kb, (uint64_t)R, 0u, ACC_ROUNDS0, fpw)
+                      : 0u;
+  bool full = false;
+  // Y_{k+1} = first accepted round >= Y_k of point k.  Y only moves at points
+  // whose round Y is rejected, so jump between those with a ballot: one
+  // iteration per rejection instead of one per point.
+  uint32_t Y = 0, myY = 0, mye = 0, q = qmax, start = 0;
+  for (;;) {
+    const bool rej = (uint32_t)lane >= start && mine && !((acc >> Y) & 1u);
+    const unsigned bad = __ballot_sync(0xffffffffu, rej);
+    const uint32_t j = bad ? (uint32_t)(__ffs(bad) - 1) : qmax;
+    if ((uint32_t)lane >= start && (uint32_t)lane < j) { myY = Y; mye = 0; }
+    if (j >= qmax) break;
+    const uint32_t am = __shfl_sync(0xffffffffu, acc, (int)j) >> Y;
+    if (am == 0 && !full) {  // decode the remaining rounds and retry this point
+      if (mine) acc |= accept_mask(ws.words, base + 53u, kb, (uint64_t)R, ACC_ROUNDS0, 24u, fpw);
+      full = true;
+      continue;
     }
-    ws.acc[lane] = acc;
-  }
-  __syncwarp();
-  // warp-uniform scan over the acceptance masks
-  uint32_t Y = 0, myY = 0, mye = 0, q = qmax;
-  for (uint32_t k = 0; k < qmax; k++) {
-    const uint32_t a = Y < 24 ? ws.acc[k] >> Y : 0u;
-    if (a == 0) { q = k; break; }
-    const uint32_t e = (uint32_t)(__ffs(a) - 1);
-    if ((uint32_t)lane == k) { myY = Y; mye = e; }
+    if (am == 0) { q = j; break; }
+    const uint32_t e = (uint32_t)(__ffs(am) - 1);
+    if ((uint32_t)lane == j) { myY = Y; mye = e; }
     Y += e;
+    start = j + 1;
   }
   if (q == 0) {  // the first point's label needs more rounds than the window: serial
     if (lane == 0) parse_fy_cursor(c, ws, id, off, i0);
