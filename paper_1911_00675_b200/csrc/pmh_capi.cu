@@ -155,7 +155,7 @@ cudaError_t launch_pmin_c(const PMinArgs& a, cudaStream_t st) {
 template <bool EXPO>
 cudaError_t launch_pminhash(const PMinArgs& a, cudaStream_t st) {
   if (a.m % PM64_C == 0 && a.m / PM64_C <= PMIN_THREADS) {
-    const size_t smem = sizeof(Slot) * (size_t)a.m;
+    const size_t smem = sizeof(Slot) * (size_t)a.m + sizeof(uint2) * PM64_CQ * (PMIN_THREADS / 32);
     cudaError_t e = cudaFuncSetAttribute(pminhash64_kernel<EXPO>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -179,7 +179,16 @@ __global__ void __launch_bounds__(PMIN_THREADS) pminhash_kernel(PMinArgs a) {
 // groups prune with everyone's minima.
 // ---------------------------------------------------------------------------
 constexpr int PM64_C = 64;
-constexpr int PM64_REFRESH = 16;   // elements between threshold refreshes
+#ifndef PM64_REFRESH
+#define PM64_REFRESH 16    // elements between threshold refreshes
+#endif
+#ifndef PM64_USEQ
+#define PM64_USEQ 1        // per-warp candidate queue
+#endif
+#ifndef PM64_TCONST
+#define PM64_TCONST 8.0    // threshold guess (ln m + c) / W
+#endif
+constexpr int PM64_CQ = 128;       // queued candidates per warp
 
 // Shared table layout: component k = 64 t + q (thread t, draw q) lives at
 // TRANSPOSED index q * tpg + t, so the 16..32 threads of a warp touch
@@ -189,33 +198,50 @@ __device__ __forceinline__ int64_t pm64_slot(int64_t t, int q, int tpg) {
   return (int64_t)q * tpg + t;
 }
 
-// exact path for the flagged draws of one element (rare)
+// exact check of draw q of thread t for element e (1-2 stream words and a
+// compare against the slot's own minimum; the log only when that passes)
+template <bool EXPO>
+__device__ __forceinline__ void pm64_check(uint64_t id, double winv, uint32_t e, int64_t t,
+                                           int q, int tpg, Slot* table) {
+  const uint64_t bitpos = 53ULL * (uint64_t)(t * PM64_C + q);
+  const uint64_t wi = bitpos >> 6;
+  const uint32_t sh = (uint32_t)(bitpos & 63);
+  const uint64_t lo = stream_word(id, wi + 1);
+  uint64_t b = lo >> sh;
+  if (sh > 11) b |= stream_word(id, wi + 2) << (64 - sh);
+  b &= (1ULL << 53) - 1ULL;
+  Slot* sl = &table[pm64_slot(t, q, tpg)];
+  const double cur = __longlong_as_double((long long)*(volatile unsigned long long*)&sl->h);
+  double h;
+  if constexpr (EXPO) {
+    if (exp1_scaled_lower_bound(winv, b) > cur) return;
+    h = winv * exp1_from_bits(b);
+  } else {
+    h = (double)b * INV53;
+  }
+  if (h <= cur) slot_offer(sl, h, (unsigned long long)e);
+}
+
+// exact path for all flagged draws of one element (the divergent fallback:
+// a group's first elements, while its threshold is still infinite)
 template <bool EXPO>
 __device__ __noinline__ void pm64_candidates(uint64_t cand, uint64_t id, double w, uint32_t e,
                                              int64_t t, int tpg, Slot* table) {
   const double winv = EXPO ? 1.0 / w : 1.0;
-  const int64_t k0 = t * PM64_C;
   while (cand) {
     const int q = __ffsll((long long)cand) - 1;
     cand &= cand - 1;
-    const uint64_t bitpos = 53ULL * (uint64_t)(k0 + q);
-    const uint64_t wi = bitpos >> 6;
-    const uint32_t sh = (uint32_t)(bitpos & 63);
-    const uint64_t lo = stream_word(id, wi + 1);
-    uint64_t b = lo >> sh;
-    if (sh > 11) b |= stream_word(id, wi + 2) << (64 - sh);
-    b &= (1ULL << 53) - 1ULL;
-    Slot* sl = &table[pm64_slot(t, q, tpg)];
-    const double cur = __longlong_as_double((long long)*(volatile unsigned long long*)&sl->h);
-    double h;
-    if constexpr (EXPO) {
-      if (exp1_scaled_lower_bound(winv, b) > cur) continue;
-      h = winv * exp1_from_bits(b);
-    } else {
-      h = (double)b * INV53;
-    }
-    if (h <= cur) slot_offer(sl, h, (unsigned long long)e);
+    pm64_check<EXPO>(id, winv, e, t, q, tpg, table);
   }
+}
+
+// one queued candidate per lane: (element, t << 6 | q)
+template <bool EXPO>
+__device__ __noinline__ void pm64_check_entry(uint2 en, const uint64_t* ids, const double* ws,
+                                              int tpg, Slot* table) {
+  const uint64_t id = __ldg(&ids[en.x]);
+  const double winv = (EXPO && ws) ? 1.0 / __ldg(&ws[en.x]) : 1.0;
+  pm64_check<EXPO>(id, winv, en.x, (int64_t)(en.y >> 6), (int)(en.y & 63u), tpg, table);
 }
 
 __device__ __forceinline__ double pm64_tmax(const Slot* table, int64_t t, int tpg) {
@@ -232,6 +258,23 @@ __device__ __forceinline__ double pm64_tmax(const Slot* table, int64_t t, int tp
 // Each group of tpg = m/64 threads walks its elements g, g + G, ... straight
 // from global memory (broadcast loads, next element prefetched): no block
 // barrier inside a set, so warps with more candidates do not stall the CTA.
+// st + (chi:clo): the low word on the ALU with carry-out, the high word as a
+// multiply-add with carry-in (IMAD.X, FMA pipe).  `one` is 1 loaded from
+// shared memory per element, so ptxas can neither fold nor hoist the product.
+template <uint32_t CLO, uint32_t CHI>
+__device__ __forceinline__ uint64_t add_fma_t(uint64_t st, uint32_t one) {
+  uint64_t z;
+  asm("{\n\t.reg .u32 l, h, sl, sh;\n\t"
+      "mov.b64 {sl, sh}, %2;\n\t"
+      "add.cc.u32 l, sl, %3;\n\t"
+      "madc.lo.u32 h, %1, %4, sh;\n\t"
+      "mov.b64 %0, {l, h};\n\t}"
+      : "=l"(z) : "r"(one), "l"(st), "n"(CLO), "n"(CHI));
+  return z;
+}
+#define add_fma(st, one, clo, chi) add_fma_t<clo, chi>(st, one)
+
+
 #ifndef PM64_MINBLOCKS
 #define PM64_MINBLOCKS 4   // 64 registers, 4 CTAs (32 warps) per SM
 #endif
@@ -246,6 +289,11 @@ __global__ void __launch_bounds__(PMIN_THREADS, PM64_MINBLOCKS) pminhash64_kerne
   Slot* table = reinterpret_cast<Slot*>(smem);
   const double two53m = 9007199254740992.0 * 1.0000000000009095;  // 2^53 (1 + 2^-40)
   const uint64_t wbase = 53ULL * (uint64_t)t + 1ULL;                // first word (1-based)
+  __shared__ uint32_t s_one;
+  __shared__ double s_wsum[PMIN_THREADS / 32];
+  __shared__ int s_retry;
+  if (threadIdx.x == 0) s_one = 1u;
+  __syncthreads();
 
   for (int64_t bs = blockIdx.x; bs < a.nsets; bs += gridDim.x) {
     const int64_t s = a.order ? (int64_t)a.order[bs] : bs;
@@ -255,56 +303,139 @@ __global__ void __launch_bounds__(PMIN_THREADS, PM64_MINBLOCKS) pminhash64_kerne
       if (threadIdx.x == 0) atomicMin(a.err_set, (long long)s);
       continue;
     }
-    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-      table[k].h = EMPTY_H;
-      table[k].idx = EMPTY_IDX;
+    // Threshold guess: every slot minimum is Exp(W) (W = total weight), so
+    // tg = (ln m + PM64_TCONST) / W bounds all m of them unless a rare set
+    // (~m e^-(ln m + c) = e^-c) exceeds it; the final table is verified and
+    // such a set re-runs with 4 tg, then without a bound.  Draws above tg are
+    // never candidates, so no element starts with an infinite threshold.
+    double W;
+    if (EXPO && a.w) {
+      double p = 0.0;
+      for (int64_t k = threadIdx.x; k < n; k += blockDim.x) p += __ldg(&a.w[off + k]);
+      for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+      if ((threadIdx.x & 31) == 0) s_wsum[threadIdx.x >> 5] = p;
+      __syncthreads();
+      W = 0.0;
+      for (int k = 0; k < PMIN_THREADS / 32; k++) W += s_wsum[k];
+    } else {
+      W = (double)n;
     }
-    __syncthreads();
-    if (active) {
-      const uint64_t* ids = a.ids + off;
-      const double* ws = (EXPO && a.w) ? a.w + off : nullptr;
-      double tmax = __longlong_as_double(0x7FF0000000000000LL);
-      int since = 0;
-      // groups per warp (2 when m = 1024): the trip count is made warp-uniform
-      // so a full-warp __syncwarp can reconverge the lanes every element
-      const int gpw = tpg >= 32 ? 1 : 32 / tpg;
-      const int gsub = g % gpw;
-      int64_t ew = g - gsub;                       // first group of this warp
-      int64_t e = ew + gsub;
-      uint64_t id_n = e < n ? __ldg(&ids[e]) : 0;
-      double w_n = (ws && e < n) ? __ldg(&ws[e]) : 1.0;
-      for (; ew < n; ew += groups) {
-        e = ew + gsub;
-        const bool live = e < n;
-        const uint64_t id = id_n;
-        const double w = w_n;
-        if (e + groups < n) {                      // prefetch the next element
-          id_n = __ldg(&ids[e + groups]);
-          if (ws) w_n = __ldg(&ws[e + groups]);
-        }
-        const double tb = tmax * (w * two53m);
-        // b < Tb = floor(tb) + 1  =>  b >> 21 <= tb >> 21
-        const uint32_t tbh = tb < 9007199254740992.0 ? (uint32_t)((uint64_t)tb >> 21)
-                                                      : 0xFFFFFFFFu;
-        uint64_t st = id + wbase * GOLDEN;
-        uint32_t c_lo = 0, c_hi = 0;
-        const uint32_t k4 = a.k4;
+    const double inf_d = __longlong_as_double(0x7FF0000000000000LL);
+    double tg = (log((double)m) + PM64_TCONST) / W;
+    if (!(tg > 0.0) || !(tg < 1e300)) tg = inf_d;
+    for (int attempt = 0;; attempt++) {
+      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+        table[k].h = EMPTY_H;
+        table[k].idx = EMPTY_IDX;
+      }
+      __syncthreads();
+      if (active) {
+        const uint64_t* ids = a.ids + off;
+        const double* ws = (EXPO && a.w) ? a.w + off : nullptr;
+        double tmax = tg;
+        int since = 0;
+        // groups per warp (2 when m = 1024): the trip count is made warp-uniform
+        // so a full-warp __syncwarp can reconverge the lanes every element
+        const int gpw = tpg >= 32 ? 1 : 32 / tpg;
+        const int gsub = g % gpw;
+        int64_t ew = g - gsub;                       // first group of this warp
+        int64_t e = ew + gsub;
+        // per-warp candidate queue (warp-aligned groups only: the trip count
+        // and every lane must be warp-uniform for the collectives)
+        const bool use_q = PM64_USEQ && ((32 % tpg == 0) || (tpg % 32 == 0));
+        const int lane = threadIdx.x & 31;
+        uint2* cq = reinterpret_cast<uint2*>(smem + sizeof(Slot) * m) + (threadIdx.x >> 5) * PM64_CQ;
+        int qn = 0;
+        uint64_t id_n = e < n ? __ldg(&ids[e]) : 0;
+        double w_n = (ws && e < n) ? __ldg(&ws[e]) : 1.0;
+        for (; ew < n; ew += groups) {
+          e = ew + gsub;
+          const bool live = e < n;
+          const uint64_t id = id_n;
+          const double w = w_n;
+          if (e + groups < n) {                      // prefetch the next element
+            id_n = __ldg(&ids[e + groups]);
+            if (ws) w_n = __ldg(&ws[e + groups]);
+          }
+          const double tb = tmax * (w * two53m);
+          // b < Tb = floor(tb) + 1  =>  b >> 21 <= tb >> 21
+          const uint32_t tbh = tb < 9007199254740992.0 ? (uint32_t)((uint64_t)tb >> 21)
+                                                        : 0xFFFFFFFFu;
+          uint64_t st = id + wbase * GOLDEN;
+          const uint32_t one = *(volatile uint32_t*)&s_one;
+          uint32_t c_lo = 0, c_hi = 0;
+          const uint32_t k4 = a.k4;
+#define MIX mix64
 #include "pm64_body.inc"
-        const uint64_t cand = live ? (((uint64_t)c_hi << 32) | c_lo) : 0ULL;
-        // candidates are cheap (1-2 stream words + a compare against the
-        // slot's own minimum); the threshold refresh is periodic -- a stale,
-        // larger tmax only admits more candidates
-        if (cand) pm64_candidates<EXPO>(cand, id, w, (uint32_t)e, t, tpg, table);
-        if (++since >= PM64_REFRESH || (cand && !(tmax < 1e300))) {
-          tmax = pm64_tmax(table, t, tpg);
-          since = 0;
+#undef MIX
+          const uint64_t cand = live ? (((uint64_t)c_hi << 32) | c_lo) : 0ULL;
+          // candidates are cheap (1-2 stream words + a compare against the
+          // slot's own minimum) but scattered: a few lanes per warp-step.  They
+          // are queued per warp and checked 32 at a time with every lane busy;
+          // only the all-candidate start (infinite threshold) or a queue
+          // overflow runs them in place.  The threshold refresh is periodic --
+          // a stale, larger tmax only admits more candidates.
+          const bool inf = !(tmax < 1e300);
+          if (use_q) {
+            const int c = __popcll(cand);
+            int x = c;                                   // inclusive lane scan
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int y = __shfl_up_sync(0xffffffffu, x, o);
+              if (lane >= o) x += y;
+            }
+            const int total = __shfl_sync(0xffffffffu, x, 31);
+            const bool direct = __any_sync(0xffffffffu, inf) || qn + total > PM64_CQ;
+            if (direct) {
+              if (cand) pm64_candidates<EXPO>(cand, id, w, (uint32_t)e, t, tpg, table);
+            } else if (total) {
+              int pos = qn + x - c;
+              for (uint64_t cb = cand; cb; cb &= cb - 1)
+                cq[pos++] = make_uint2((uint32_t)e, ((uint32_t)t << 6) | (uint32_t)(__ffsll((long long)cb) - 1));
+              qn += total;
+              __syncwarp();
+              while (qn >= 32) {
+                qn -= 32;
+                const uint2 en = cq[qn + lane];
+                __syncwarp();
+                pm64_check_entry<EXPO>(en, ids, ws, tpg, table);
+              }
+            }
+          } else if (cand) {
+            pm64_candidates<EXPO>(cand, id, w, (uint32_t)e, t, tpg, table);
+          }
+          if (++since >= PM64_REFRESH || (cand && inf)) {
+            tmax = fmin(pm64_tmax(table, t, tpg), tg);
+            since = 0;
+          }
+          // reconverge: lanes that took the candidate path would otherwise run
+          // the straight-line body out of phase (independent thread scheduling)
+          __syncwarp();
         }
-        // reconverge: lanes that took the candidate path would otherwise run
-        // the straight-line body out of phase (independent thread scheduling)
-        __syncwarp();
+        if (use_q && lane < qn) pm64_check_entry<EXPO>(cq[lane], ids, ws, tpg, table);
+      }
+      __syncthreads();
+      // verification: every slot filled and <= tg
+      {
+        unsigned long long mx = 0;
+        for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+          const unsigned long long h = table[k].h;
+          mx = h > mx ? h : mx;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
+          mx = v > mx ? v : mx;
+        }
+        if (threadIdx.x == 0) s_retry = 0;
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0 && __longlong_as_double((long long)mx) > tg) atomicOr(&s_retry, 1);
+        __syncthreads();
+        const int retry = s_retry;
+        __syncthreads();
+        if (!retry || !(tg < 1e300)) break;
+        tg = attempt >= 1 ? inf_d : tg * 4.0;
       }
     }
-    __syncthreads();
     uint64_t* sig = a.sig + (size_t)s * m;
     for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
       const unsigned long long bi = table[pm64_slot(k / PM64_C, (int)(k % PM64_C), tpg)].idx;
