@@ -143,6 +143,20 @@ int pmh_bbit(const uint64_t* sig, int64_t nsets, int64_t m, int b,
              int64_t* out, void* stream);
 
 /*
+ * Fused MSE cell: replaces K._k_mse_cell(algo, m, wa, wb, seed, s) (K:920-963,
+ * called by harness.run_mse_cell harness.py:266-280).  For each of s pairs
+ * the ids come from ONE splitmix64 stream seeded with `seed` (pair t, weight
+ * pair q -> word t*npairs + q), side A holds the q with wa[q] > 0, side B the
+ * q with wb[q] > 0; both are sketched with `algo` at m and their equal
+ * components counted into matches[t] (HOST int64[s]).  wa/wb are HOST
+ * arrays.  Generation, sketching and counting run on the device in chunks;
+ * synchronous on `stream`.  Errors as pmh_sketch_csr (an all-zero side ->
+ * PMH_ERR_EMPTY).
+ */
+int pmh_mse_cell(int algo, int64_t m, const double* wa, const double* wb, int64_t npairs,
+                 uint64_t seed, int64_t s, int64_t* matches, void* stream);
+
+/*
  * Diagnostic: measured 32-bit ALU-pipe peak of the current device in Gop/s
  * (8 independent LOP3 chains per thread, full occupancy) -- the roofline
  * denominator for the integer-bound signature kernels.  Synchronous.

@@ -198,3 +198,22 @@ def trunc_exp_consts(lam):
     out = np.empty(3, np.float64)
     lib().orc_trunc_exp_consts(lam, _p(out, _f64p))
     return tuple(float(v) for v in out)
+
+
+def mse_cell(algo, m, wa, wb, seed, s, threads=8):
+    """K._k_mse_cell (K:920-963) restated: pair t, weight pair q takes stream
+    word t*npairs + q of RandomStream(seed) as its id; side A keeps the q with
+    wa[q] > 0, side B those with wb[q] > 0 (q order); both sides are sketched
+    and equal components counted -> int64[s]."""
+    wa = np.asarray(wa, np.float64)
+    wb = np.asarray(wb, np.float64)
+    P = wa.size
+    words = stream_words(seed, s * P).reshape(s, P)
+    ma, mb = wa > 0, wb > 0
+    na, nb = int(ma.sum()), int(mb.sum())
+    ids = np.concatenate([words[:, ma].ravel(), words[:, mb].ravel()])
+    w = np.concatenate([np.tile(wa[ma], s), np.tile(wb[mb], s)])
+    off = np.concatenate([np.arange(s + 1, dtype=np.int64) * na,
+                          s * na + np.arange(1, s + 1, dtype=np.int64) * nb])
+    sig, _ = sketch_csr(algo, m, ids, w, off, threads=threads)
+    return (sig[:s] == sig[s:]).sum(axis=1).astype(np.int64)

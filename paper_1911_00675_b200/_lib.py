@@ -36,7 +36,7 @@ UNWEIGHTED_IDS = {10, 11, 12, 13, 14, 15, 16, 17, 18}
 EXPORTS = ("pmh_version", "pmh_last_error", "pmh_sketch_csr", "pmh_sketch_csr_async",
            "pmh_status_reset", "pmh_status_check", "pmh_sketch_csr_host", "pmh_sketch_csr_host_multi",
            "pmh_count_equal", "pmh_allpairs_tile", "pmh_allpairs_hist", "pmh_bbit",
-           "pmh_probe_alu_peak")
+           "pmh_mse_cell", "pmh_probe_alu_peak")
 
 _lib = None
 _lock = threading.Lock()
@@ -89,6 +89,9 @@ def load():
         L.pmh_allpairs_hist.restype = ctypes.c_int
         L.pmh_bbit.argtypes = [_vp, _i64, _i64, ctypes.c_int, _vp, _vp]
         L.pmh_bbit.restype = ctypes.c_int
+        L.pmh_mse_cell.argtypes = [ctypes.c_int, _i64, _vp, _vp, _i64, ctypes.c_uint64, _i64,
+                                   _vp, _vp]
+        L.pmh_mse_cell.restype = ctypes.c_int
         L.pmh_probe_alu_peak.argtypes = [ctypes.POINTER(ctypes.c_double),
                                          ctypes.POINTER(ctypes.c_double)]
         L.pmh_probe_alu_peak.restype = ctypes.c_int

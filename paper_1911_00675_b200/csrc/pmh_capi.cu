@@ -23,6 +23,7 @@
 #include "pmh_order.cuh"
 #include "pmh_probe.cuh"
 #include "pmh_baselines.cuh"
+#include "pmh_harness.cuh"
 
 using namespace pmh;
 
@@ -648,6 +649,95 @@ int pmh_bbit(const uint64_t* sig, int64_t nsets, int64_t m, int b, int64_t* out,
   bbit_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(sig, total, m, b, out);
   PMH_CUDA(cudaGetLastError());
   return PMH_OK;
+}
+
+int pmh_mse_cell(int algo, int64_t m, const double* wa, const double* wb, int64_t npairs,
+                 uint64_t seed, int64_t s, int64_t* matches, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (npairs < 1 || !wa || !wb) return set_error(PMH_ERR_INVALID, "fixture needs >= 1 weight pair");
+  if (s < 0) return set_error(PMH_ERR_INVALID, "negative pair count");
+  int vrc = validate_sketch(algo, m, wa, 1);
+  if (vrc != PMH_OK) return vrc;
+  if (s == 0) return PMH_OK;
+  if (!matches) return set_error(PMH_ERR_INVALID, "matches buffer required");
+  // element ranks of each side (K:944-955: q order)
+  std::vector<int32_t> ra((size_t)npairs), rb((size_t)npairs);
+  int64_t na = 0, nb = 0;
+  for (int64_t q = 0; q < npairs; q++) {
+    if (!(wa[q] >= 0.0) || !(wb[q] >= 0.0) || !(wa[q] > 0.0 || wb[q] > 0.0))
+      return set_error(PMH_ERR_INVALID, "each pair needs a positive coordinate and no negatives");
+    ra[(size_t)q] = (int32_t)na;
+    rb[(size_t)q] = (int32_t)nb;
+    na += wa[q] > 0.0;
+    nb += wb[q] > 0.0;
+  }
+  if (na == 0 || nb == 0) return set_error(PMH_ERR_EMPTY, "cannot sketch an empty set");
+  // pairs per chunk: bound the device working set to ~512 MB
+  const int64_t per_pair = 16 * (na + nb) + 16 * m + 28;
+  int64_t C = (512LL << 20) / per_pair;
+  C = C < 1 ? 1 : (C > s ? s : C);
+  C = C > (1LL << 30) ? (1LL << 30) : C;
+  if (const char* ev = getenv("PMH_MSE_CHUNK_PAIRS")) {  // test hook: force chunking
+    const long long cap = atoll(ev);
+    if (cap > 0 && cap < C) C = cap;
+  }
+  ensure_pool_retained();
+  double *d_wa = nullptr, *d_wb = nullptr, *d_w = nullptr;
+  int32_t *d_ra = nullptr, *d_rb = nullptr, *d_cnt = nullptr;
+  uint64_t *d_ids = nullptr, *d_sig = nullptr;
+  int64_t *d_off = nullptr, *d_match = nullptr, *d_status = nullptr;
+  int rc = PMH_OK;
+  auto alloc = [&](void** p, size_t bytes) {
+    if (rc != PMH_OK) return;
+    cudaError_t e = cudaMallocAsync(p, bytes, st);
+    if (e != cudaSuccess) rc = set_error(PMH_ERR_NOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+  };
+  alloc((void**)&d_wa, sizeof(double) * npairs);
+  alloc((void**)&d_wb, sizeof(double) * npairs);
+  alloc((void**)&d_ra, sizeof(int32_t) * npairs);
+  alloc((void**)&d_rb, sizeof(int32_t) * npairs);
+  alloc((void**)&d_ids, sizeof(uint64_t) * C * (na + nb));
+  alloc((void**)&d_w, sizeof(double) * C * (na + nb));
+  alloc((void**)&d_off, sizeof(int64_t) * (2 * C + 1));
+  alloc((void**)&d_sig, sizeof(uint64_t) * 2 * C * m);
+  alloc((void**)&d_cnt, sizeof(int32_t) * C);
+  alloc((void**)&d_match, sizeof(int64_t) * s);
+  alloc((void**)&d_status, 16);
+  if (rc == PMH_OK) {
+    cudaMemcpyAsync(d_wa, wa, sizeof(double) * npairs, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_wb, wb, sizeof(double) * npairs, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_ra, ra.data(), sizeof(int32_t) * npairs, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_rb, rb.data(), sizeof(int32_t) * npairs, cudaMemcpyHostToDevice, st);
+    rc = pmh_status_reset(d_status, st);
+  }
+  for (int64_t t0 = 0; rc == PMH_OK && t0 < s; t0 += C) {
+    const int64_t c = s - t0 < C ? s - t0 : C;
+    MseGenArgs g{d_wa, d_wb, d_ra, d_rb, npairs, na, nb, seed, t0, c, d_ids, d_w, d_off};
+    int64_t blocks = (c * npairs + 255) / 256;
+    blocks = blocks < 1 ? 1 : (blocks > 148 * 16 ? 148 * 16 : blocks);
+    mse_gen_kernel<<<(unsigned)blocks, 256, 0, st>>>(g);
+    if (cudaGetLastError() != cudaSuccess) { rc = set_error(PMH_ERR_CUDA, "mse_gen_kernel launch"); break; }
+    rc = pmh_sketch_csr_async(algo, m, d_ids, d_w, d_off, 2 * c, d_sig, nullptr, d_status, st);
+    if (rc != PMH_OK) break;
+    rc = pmh_count_equal(d_sig, d_sig + (size_t)c * m, c, m, d_cnt, st);
+    if (rc != PMH_OK) break;
+    int64_t wb_ = (c + 255) / 256;
+    wb_ = wb_ > 148 * 16 ? 148 * 16 : wb_;
+    widen_counts_kernel<<<(unsigned)wb_, 256, 0, st>>>(d_cnt, c, d_match + t0);
+  }
+  if (rc == PMH_OK) {
+    int64_t err = -1;
+    rc = pmh_status_check(d_status, &err, st);
+  }
+  if (rc == PMH_OK) {
+    cudaError_t e = cudaMemcpyAsync(matches, d_match, sizeof(int64_t) * s, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = set_error(PMH_ERR_CUDA, std::string("mse cell: ") + cudaGetErrorString(e));
+  }
+  void* bufs[] = {d_wa, d_wb, d_ra, d_rb, d_ids, d_w, d_off, d_sig, d_cnt, d_match, d_status};
+  for (void* b : bufs)
+    if (b) cudaFreeAsync(b, st);
+  return rc;
 }
 
 int pmh_probe_alu_peak(double* gops_out, double* ms_out) {

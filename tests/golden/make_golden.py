@@ -194,5 +194,36 @@ def main():
     save("bbit", **arrays)
 
 
+def main_mse():
+    # 6) harness MSE cells (K:920-963 via harness.run_mse_cell, harness.py:266-280):
+    # raw match counts per cell and the reference's finished MseRow values
+    from probminhash import harness as H
+    arrays = {}
+    cells = []
+    for algo in H.ALGORITHM_IDS:
+        for fixture in ("skew2", "binary3", "tenth10", "binary64", "pareto16", "single1",
+                        "disjoint2"):
+            if algo in H.UNWEIGHTED_ALGORITHMS and fixture in ("skew2", "pareto16"):
+                continue
+            for m in (16, 64):
+                cells.append((algo, m, fixture))
+    for ci, (algo, m, fixture) in enumerate(cells):
+        V = H.FIXTURES[fixture]
+        wa, wb = V.arrays()
+        seed = H.cell_seed(7, "mse", algo, m, fixture)
+        s = 40
+        arrays[f"m{ci}_matches"] = K._k_mse_cell(H.ALGORITHM_IDS[algo], m, wa, wb,
+                                                 np.uint64(seed), s)
+        arrays[f"m{ci}_key"] = np.array([algo, fixture])
+        arrays[f"m{ci}_ms"] = np.array([m, s, seed], np.uint64)
+        row = H.run_mse_cell(algo, m, fixture, s, 7)
+        arrays[f"m{ci}_row"] = np.array([row.jp, row.mse, row.relative_mse, row.zscore])
+    save("mse", **arrays)
+
+
 if __name__ == "__main__":
-    main()
+    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "mse":
+        main_mse()
+    else:
+        main()
+        main_mse()
