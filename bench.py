@@ -45,8 +45,10 @@ METRIC = "set elements hashed/sec at m=1024"
 # a 53-bit draw uses 53/64 word, + 2 ops (extract 32 bits, compare)
 ALU_OPS_PER_DRAW = 14.0 * 53.0 / 64.0 + 2.0
 # dram read+write bytes per launch from `ncu --set full` of the full config-2
-# launch (profiles/r01_ncu_pminhash64_full.txt); None until captured
-TRAFFIC_BYTES = {"pminhash": 1447215000 + 34147328}
+# launch (profiles/r01_ncu_pminhash64_full_config2.txt); the read side exceeds
+# the algorithmic 1.39 GB of ids/weights by the weight-sum pre-pass of the
+# threshold guess (~0.7 GB, a second read of the weights)
+TRAFFIC_BYTES = {"pminhash": 2182183000 + 52388864}
 UNIT = "elements/s"
 
 
