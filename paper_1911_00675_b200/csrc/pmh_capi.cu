@@ -244,7 +244,14 @@ int get_aux(AuxStream** out) {
   auto it = g_aux.find(dev);
   if (it == g_aux.end()) {
     AuxStream a;
-    PMH_CUDA(cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking));
+    // highest priority: the small-set kernel's (few, latency-bound) CTAs are
+    // placed before the pending CTAs of the big kernel, so they run beside it
+    // from the start instead of as a tail
+    int least = 0, greatest = 0;
+    PMH_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    const char* ev = getenv("PMH_AUX_PRIO");
+    const int prio = (ev && ev[0] == '0') ? least : greatest;
+    PMH_CUDA(cudaStreamCreateWithPriority(&a.s, cudaStreamNonBlocking, prio));
     PMH_CUDA(cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming));
     PMH_CUDA(cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming));
     it = g_aux.emplace(dev, a).first;
@@ -395,23 +402,34 @@ int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
     if (rc) { cudaFreeAsync(order_ws, st); return rc; }
     PMH_CUDA(cudaEventRecord(aux->fork, st));
     PMH_CUDA(cudaStreamWaitEvent(aux->s, aux->fork, 0));
-    switch (fam) {
-      case FAM_PMH1: e = launch_family<FAM_PMH1>(a, st); break;
-      case FAM_PMH2: e = launch_family<FAM_PMH2>(a, st); break;
-      case FAM_PMH3: e = launch_family<FAM_PMH3>(a, st); break;
-      case FAM_PMH4: e = launch_family<FAM_PMH4>(a, st); break;
-      case FAM_UW3: e = launch_family<FAM_UW3>(a, st); break;
-      default: e = launch_family<FAM_UW4>(a, st); break;
-    }
-    if (e == cudaSuccess) {
+    auto big = [&]() {
       switch (fam) {
-        case FAM_PMH1: e = launch_small<FAM_PMH1>(a, aux->s); break;
-        case FAM_PMH2: e = launch_small<FAM_PMH2>(a, aux->s); break;
-        case FAM_PMH3: e = launch_small<FAM_PMH3>(a, aux->s); break;
-        case FAM_PMH4: e = launch_small<FAM_PMH4>(a, aux->s); break;
-        case FAM_UW3: e = launch_small<FAM_UW3>(a, aux->s); break;
-        default: e = launch_small<FAM_UW4>(a, aux->s); break;
+        case FAM_PMH1: return launch_family<FAM_PMH1>(a, st);
+        case FAM_PMH2: return launch_family<FAM_PMH2>(a, st);
+        case FAM_PMH3: return launch_family<FAM_PMH3>(a, st);
+        case FAM_PMH4: return launch_family<FAM_PMH4>(a, st);
+        case FAM_UW3: return launch_family<FAM_UW3>(a, st);
+        default: return launch_family<FAM_UW4>(a, st);
       }
+    };
+    auto small = [&]() {
+      switch (fam) {
+        case FAM_PMH1: return launch_small<FAM_PMH1>(a, aux->s);
+        case FAM_PMH2: return launch_small<FAM_PMH2>(a, aux->s);
+        case FAM_PMH3: return launch_small<FAM_PMH3>(a, aux->s);
+        case FAM_PMH4: return launch_small<FAM_PMH4>(a, aux->s);
+        case FAM_UW3: return launch_small<FAM_UW3>(a, aux->s);
+        default: return launch_small<FAM_UW4>(a, aux->s);
+      }
+    };
+    // the small-set kernel first (see get_aux)
+    static const bool small_first = !(getenv("PMH_SMALL_FIRST") && getenv("PMH_SMALL_FIRST")[0] == '0');
+    if (small_first) {
+      e = small();
+      if (e == cudaSuccess) e = big();
+    } else {
+      e = big();
+      if (e == cudaSuccess) e = small();
     }
     cudaEventRecord(aux->join, aux->s);
     cudaStreamWaitEvent(st, aux->join, 0);

@@ -14,6 +14,9 @@
 namespace pmh {
 
 constexpr double HEAVY_POINTS = 8.0;   // expected points above which mode B runs
+#ifndef PMH_L2_PREFETCH
+#define PMH_L2_PREFETCH 1
+#endif
 
 // Division-free prefilter for the common case of large sets: decide from the
 // element's first stream word whether its FIRST point exceeds thr and the
@@ -23,8 +26,8 @@ constexpr double HEAVY_POINTS = 8.0;   // expected points above which mode B run
 // x = fl(fl(1/w) * E) (E >= U for PMH1/2; T exact for PMH3/4), so a rejection
 // here is always a rejection there.  Returns false when unsure.
 template <int F>
-__device__ __forceinline__ bool first_point_rejects(const SetCtx& c, const Tables& T, uint64_t id,
-                                                    double w, double thr) {
+__device__ __forceinline__ bool first_point_rejects(const Tables& T, uint64_t id, double w,
+                                                    double thr) {
   const uint64_t b53 = mix64(id + GOLDEN) & ((1ULL << 53) - 1ULL);  // bits 0..52 = word 1
   const double U = (double)b53 * INV53;
   const double lo = 0.99999999999909051, hi = 1.0000000000009095;  // 1 -/+ 2^-40
@@ -76,100 +79,111 @@ struct LocalGrab {
   __device__ __forceinline__ unsigned next(int) { const unsigned b = cur; cur += chunk; return b; }
 };
 
+// One batch of up to 32 queued survivors, one per lane (mode A), then the
+// batch's warp-cooperative elements (mode B) and the h_max refresh.  Kept out
+// of line so the register budget of the heavy recurrences does not spill the
+// streaming prefilter loop around it (one call per batch, i.e. per ~4-32
+// prefilter iterations).  Returns true if an element hit a loop cap.
+template <int F>
+__device__ __forceinline__ bool run_batch(SetCtx& c, const Tables& T, const uint64_t* ids,
+                                       const double* w, WarpScratch* wscr, uint32_t* fy_dense,
+                                       bool warp_ok, int lane, int take, int qn) {
+  bool failed = false;
+  const bool act = lane < take;
+  const int64_t e = act ? (int64_t)wscr->sq[qn - take + lane] : 0;   // LIFO: the queue's tail
+  __syncwarp();
+  const int64_t upd0 = c.updates;
+  bool heavy = false;
+  int status = EL_DONE;
+  if (act) {
+    const uint64_t id = __ldg(&ids[e]);
+    double winv = 1.0;
+    if (family_weighted(F) && w) winv = 1.0 / __ldg(&w[e]);
+    heavy = warp_ok && ctx_thr(c) > HEAVY_POINTS * winv;
+    if (!heavy) {
+      SparseFY fy; fy.reset();
+      status = run_element<F>(c, T, fy, e, id, winv);
+    }
+  }
+  if (status == EL_FAIL) failed = true;
+  unsigned hm = __ballot_sync(0xffffffffu, act && (heavy || status == EL_NEED_WARP));
+  // warp-cooperative elements of this batch, one at a time
+  while (hm) {
+    const int l = __ffs(hm) - 1;
+    hm &= hm - 1;
+    const int64_t eh = __shfl_sync(0xffffffffu, e, l);
+    const uint64_t idh = __ldg(&ids[eh]);
+    const double winvh = (family_weighted(F) && w) ? 1.0 / __ldg(&w[eh]) : 1.0;
+    const int st = warp_element<F>(c, T, *wscr, fy_dense, lane, eh, idh, winvh);
+    if (st == EL_FAIL) failed = true;
+    if (lane == 0) c.multi++;
+    __syncwarp();
+  }
+  // refresh h_max after batches that lowered a slot (and every 8th)
+  const bool changed = __any_sync(0xffffffffu, c.updates != upd0);
+  if (changed || ++c.since_refresh >= 8) {
+    hmax_refresh_warp(c, lane);
+    c.since_refresh = 0;
+  }
+  return failed;
+}
+
+// The streaming loop: each lane takes PMH_EPL elements per chunk (chunk =
+// 32 * PMH_EPL, coalesced per j), so the per-chunk costs (grab, stop-limit
+// read, ballots, queue append, loop control) are amortised and PMH_EPL
+// independent loads and prefilters are in flight per lane.  The ids are in
+// L2 (prefetched per set) and the weights too (the weight sum), so no
+// register prefetch is kept across the heavy batch.  32-bit element indices
+// (sets hold < 2^31 elements); rejections counted in a register (stats only).
+#ifndef PMH_EPL
+#define PMH_EPL 4
+#endif
 template <int F, class Grab>
 __device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const uint64_t* ids,
                                            const double* w, int64_t n, int64_t chunk, Grab& grab,
                                            WarpScratch* wscr, uint32_t* fy_dense, bool warp_ok,
                                            bool& failed, int lane) {
-  unsigned base = grab.next(lane);
-  uint64_t id_nx = 0;
-  double w_nx = 1.0;
-  {
-    const int64_t e = (int64_t)base + lane;
-    if (lane < chunk && e < n) {
-      id_nx = __ldg(&ids[e]);
-      if (family_weighted(F) && w) w_nx = __ldg(&w[e]);
-    }
-  }
-  int since_refresh = 0;
+  const volatile unsigned long long* hb = c.hmax_bits;
+  const double tg = c.tguess;
+  const uint32_t n32 = (uint32_t)n, ch = (uint32_t)chunk;   // ch <= 32 * PMH_EPL
+  uint32_t rej = 0;                            // prefilter rejections (stats)
   int qn = 0;                                  // queued survivors (warp-uniform)
   for (;;) {
-    const bool more = (int64_t)base < n;
+    const uint32_t base = grab.next(lane);
+    const bool more = base < n32;
     if (more) {
-      const int64_t e = (int64_t)base + lane;
-      const bool active = lane < chunk && e < n;
-      const uint64_t id = id_nx;
-      const double wv = w_nx;
-      const unsigned nbase = grab.next(lane);
-      const int64_t en = (int64_t)nbase + lane;
-      if (lane < chunk && en < n) {
-        id_nx = __ldg(&ids[en]);
-        if (family_weighted(F) && w) w_nx = __ldg(&w[en]);
+      uint64_t id[PMH_EPL];
+      double wv[PMH_EPL];
+      bool act[PMH_EPL];
+#pragma unroll
+      for (int j = 0; j < PMH_EPL; j++) {
+        const uint32_t o = (uint32_t)lane + 32u * j;
+        const uint32_t e = base + o;
+        act[j] = o < ch && e < n32;
+        id[j] = act[j] ? __ldg(&ids[e]) : 0ULL;
+        wv[j] = (family_weighted(F) && w && act[j]) ? __ldg(&w[e]) : 1.0;
       }
-      bool surv = false;
-      if (active) {
-        surv = !first_point_rejects<F>(c, T, id, wv, ctx_thr(c));
-        if (!surv) c.points += (0.0 > c.tprev);          // rejected first point
+      const double hm = __longlong_as_double((long long)*hb);
+      const double thr = hm < tg ? hm : tg;
+#pragma unroll
+      for (int j = 0; j < PMH_EPL; j++) {
+        const bool surv = act[j] && !first_point_rejects<F>(T, id[j], wv[j], thr);
+        rej += act[j] && !surv;
+        const unsigned sm = __ballot_sync(0xffffffffu, surv);
+        if (surv) wscr->sq[qn + __popc(sm & ((1u << lane) - 1u))] = (int32_t)(base + (uint32_t)lane + 32u * j);
+        qn += __popc(sm);
       }
-      const unsigned sm = __ballot_sync(0xffffffffu, surv);
-      if (surv) wscr->sq[qn + __popc(sm & ((1u << lane) - 1u))] = (int32_t)e;
-      qn += __popc(sm);
-      base = nbase;
       __syncwarp();
     }
-    const int64_t upd0 = c.updates;
-    bool ran = false;
-    unsigned hm = 0;                             // lanes whose element runs warp-wide
-    int64_t e = 0;
-    if (qn >= 32 || (!more && qn > 0)) {
-      // run up to 32 queued survivors, one per lane
+    while (qn >= 32 || (!more && qn > 0)) {
       const int take = qn < 32 ? qn : 32;
-      const bool act = lane < take;
-      e = act ? (int64_t)wscr->sq[lane] : 0;
-      __syncwarp();
-      if (qn > 32 && lane < qn - 32) wscr->sq[lane] = wscr->sq[lane + 32];
+      if (run_batch<F>(c, T, ids, w, wscr, fy_dense, warp_ok, lane, take, qn)) failed = true;
       qn -= take;
       __syncwarp();
-      bool heavy = false;
-      int status = EL_DONE;
-      if (act) {
-        const uint64_t id = __ldg(&ids[e]);
-        double winv = 1.0;
-        if (family_weighted(F) && w) winv = 1.0 / __ldg(&w[e]);
-        heavy = warp_ok && ctx_thr(c) > HEAVY_POINTS * winv;
-        if (!heavy) {
-          SparseFY fy; fy.reset();
-          status = run_element<F>(c, T, fy, e, id, winv);
-        }
-      }
-      if (status == EL_FAIL) failed = true;
-      const bool want = act && (heavy || status == EL_NEED_WARP);
-      hm = __ballot_sync(0xffffffffu, want);
-      ran = true;
     }
-    // warp-cooperative elements of this batch, one at a time
-    while (hm) {
-      const int l = __ffs(hm) - 1;
-      hm &= hm - 1;
-      const int64_t eh = __shfl_sync(0xffffffffu, e, l);
-      const uint64_t idh = __ldg(&ids[eh]);
-      const double winvh = (family_weighted(F) && w) ? 1.0 / __ldg(&w[eh]) : 1.0;
-      const int st = warp_element<F>(c, T, *wscr, fy_dense, lane, eh, idh, winvh);
-      if (st == EL_FAIL) failed = true;
-      if (lane == 0) c.multi++;
-      __syncwarp();
-      ran = true;
-    }
-    if (ran) {
-      // refresh h_max after batches that lowered a slot (and every 8th)
-      const bool changed = __any_sync(0xffffffffu, c.updates != upd0);
-      if (changed || ++since_refresh >= 8) {
-        hmax_refresh_warp(c, lane);
-        since_refresh = 0;
-      }
-    }
-    if (!more && qn == 0) break;
+    if (!more) break;
   }
+  if (0.0 > c.tprev) c.points += rej;          // rejected first points
 }
 
 // Dynamic shared memory: Slot[m] | WarpScratch[nwarps] | int32 FY[nwarps][m+1]
@@ -220,6 +234,14 @@ __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS) sketch_sets_
       slots[k].h = EMPTY_H;
       slots[k].idx = EMPTY_IDX;
     }
+    // Pull the set's ids into L2 while the weights are summed (the weights
+    // arrive there by the sum itself): the element loop then prefetches one
+    // chunk ahead from L2 instead of HBM, whose latency that single chunk in
+    // flight per warp could not cover.
+#if PMH_L2_PREFETCH
+    for (int64_t L = threadIdx.x; L * 16 < n; L += blockDim.x)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(ids + L * 16));
+#endif
     double W;
     if (family_weighted(F) && w) {
       // four independent loads in flight per thread (latency-bound otherwise)
@@ -246,12 +268,12 @@ __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS) sketch_sets_
     c.m = m;
     c.kbits = bits_for(m);
     c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
-    c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0;
+    c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
     double tg = (double)m * (log((double)m) + a.tconst) / W;
     if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
     bool failed = false;
     int64_t chunk = (n + 2 * nwarps - 1) / (2 * nwarps);
-    chunk = chunk < 1 ? 1 : (chunk > 32 ? 32 : chunk);
+    chunk = chunk < 1 ? 1 : (chunk > 32 * PMH_EPL ? 32 * PMH_EPL : chunk);
 
     for (int attempt = 0;; attempt++) {
       c.tguess = tg;
@@ -389,14 +411,14 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
     c.m = m;
     c.kbits = bits_for(m);
     c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
-    c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0;
+    c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
     double tg = (double)m * (log((double)m) + a.tconst) / W;
     if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
     bool failed = false;
     for (int attempt = 0;; attempt++) {
       c.tguess = tg;
-      LocalGrab grab{0u, 32u};
-      warp_elements<F>(c, a.T, ids, w, n, 32, grab, ws, fy, warp_ok, failed, lane);
+      LocalGrab grab{0u, 32u * PMH_EPL};
+      warp_elements<F>(c, a.T, ids, w, n, 32 * PMH_EPL, grab, ws, fy, warp_ok, failed, lane);
       unsigned long long mx = 0;
       for (int64_t k = lane; k < m; k += 32) {
         const unsigned long long h = slots[k].h;

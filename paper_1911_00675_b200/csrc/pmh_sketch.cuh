@@ -50,6 +50,7 @@ struct SetCtx {
                                      // a retry counts only points above it
   int64_t updates;
   int64_t multi;                     // elements that produced > 1 point
+  int since_refresh;                 // batches since the last h_max refresh
 };
 
 __device__ __forceinline__ double ctx_thr(const SetCtx& c) {

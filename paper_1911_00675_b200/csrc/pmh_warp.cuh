@@ -36,7 +36,7 @@ struct WarpScratch {
   uint64_t next_off;    // absolute bit offset after the batch
   uint32_t epoch;       // Fisher-Yates map epoch (one per warp-processed element)
   uint32_t pad;
-  int32_t sq[64];       // survivor queue of the large-set path (element indices)
+  int32_t sq[160];      // survivor queue of the large-set path (element indices, LIFO)
   uint32_t gm[32];      // parallel Fisher-Yates: lanes whose target is i0 + k
 };
 
