@@ -30,7 +30,7 @@ struct WarpScratch {
   uint64_t words[65];   // window (64 words for the parallel FY parse, +1 guard)
   uint32_t eoff[32];    // window-relative bit offset of each point's first draw
   int32_t lab[32];      // 1-based labels
-  double tval[32];      // TruncExp values (PMH4 parse), NaN => exponential draw
+  double dbuf[32];      // per-point increments of the ordered fold
   uint32_t q;           // points parsed
   uint32_t flags;       // bit0: batch ended by a slow path; bit1: fail
   uint64_t next_off;    // absolute bit offset after the batch
@@ -92,13 +92,22 @@ __device__ __forceinline__ double warp_thr(const SetCtx& c) {
 }
 
 // inclusive ordered fold: lane p returns fl(...fl(fl(x0 + d_0) + d_1)... + d_p)
-__device__ __forceinline__ double ordered_fold(double x0, double d, int lane, uint32_t q) {
-  double acc = x0;
+// (lanes >= q: the fold of all q).  The increments go through shared memory
+// and every lane runs the same sequential chain from broadcast loads, keeping
+// the value after its own step: one LDS + one DADD + a predicated move per
+// step instead of two shuffles, a DADD and selects.
+__device__ __forceinline__ double ordered_fold(WarpScratch& ws, double x0, double d, int lane,
+                                               uint32_t q) {
+  ws.dbuf[lane] = d;
+  __syncwarp();
+  double acc = x0, mine = x0;
+#pragma unroll 8
   for (uint32_t j = 0; j < q; j++) {
-    const double v = __shfl_sync(0xffffffffu, d, j);
-    if ((int)j <= lane) acc = acc + v;
+    acc = acc + ws.dbuf[j];
+    if ((int)j == lane) mine = acc;
   }
-  return acc;
+  __syncwarp();
+  return (uint32_t)lane < q ? mine : acc;
 }
 
 // ---- labels with replacement, power-of-two m: PMH1, PMH3, uw3 -------------
@@ -133,7 +142,7 @@ __device__ int warp_el_static(SetCtx& c, const Tables& T, WarpScratch& ws, int l
     bool had_slow = false;
     if constexpr (F == FAM_PMH1) {
       const double d = in ? winv * exp1_from_bits(u) : 0.0;
-      xv = ordered_fold(x, d, lane, q);
+      xv = ordered_fold(ws, x, d, lane, q);
     } else if constexpr (F == FAM_UW3) {
       const double U = (double)u * INV53;
       xv = pt == 1 ? U : ((double)pt - 1.0) + U;
@@ -456,7 +465,7 @@ __device__ int warp_el_fy(SetCtx& c, const Tables& T, WarpScratch& ws, uint32_t*
         const double E = exp1_from_bits(u);
         d = pt == 1 ? winv * E : (winv * __ldg(&T.beta[pt])) * E;
       }
-      xv = ordered_fold(x, d, lane, q);
+      xv = ordered_fold(ws, x, d, lane, q);
     } else if constexpr (F == FAM_PMH4) {
       if (in) {
         if (pt == 1) {
