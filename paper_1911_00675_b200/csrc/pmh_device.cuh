@@ -109,10 +109,14 @@ struct Stream {
 };
 
 __host__ __device__ __forceinline__ uint32_t bits_for(int64_t n) {  // K:86-94
+#ifdef __CUDA_ARCH__
+  return n <= 1 ? 0u : 64u - (uint32_t)__clzll((long long)(n - 1));
+#else
   uint32_t k = 0;
   int64_t v = n - 1;
   while (v > 0) { v >>= 1; k++; }
   return k;
+#endif
 }
 
 // K:97-110: uniform on {0..n-1}; returns -1 when the rejection cap is hit
@@ -131,7 +135,15 @@ __device__ __forceinline__ int64_t uniform_int(Stream& st, int64_t n) {  // K:11
 }
 
 // E = -log1p(-U) given the 53 raw bits (K:120-122)
-__device__ __forceinline__ double exp1_from_bits(uint64_t b53) {
+#ifndef PMH_EXP1_NOINLINE
+#define PMH_EXP1_NOINLINE 0
+#endif
+#if PMH_EXP1_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+double exp1_from_bits(uint64_t b53) {
   return -g_log1p(-((double)b53 * INV53));
 }
 

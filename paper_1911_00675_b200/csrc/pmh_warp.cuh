@@ -93,21 +93,24 @@ __device__ __forceinline__ double warp_thr(const SetCtx& c) {
 
 // inclusive ordered fold: lane p returns fl(...fl(fl(x0 + d_0) + d_1)... + d_p)
 // (lanes >= q: the fold of all q).  The increments go through shared memory
-// and every lane runs the same sequential chain from broadcast loads, keeping
-// the value after its own step: one LDS + one DADD + a predicated move per
-// step instead of two shuffles, a DADD and selects.
+// and every lane runs the same sequential chain from broadcast loads, writing
+// each prefix back in place (all lanes store the same value: one broadcast
+// store); lane p then reads prefix p.  Per step: a DADD and a store, the
+// loads vectorised.
 __device__ __forceinline__ double ordered_fold(WarpScratch& ws, double x0, double d, int lane,
                                                uint32_t q) {
   ws.dbuf[lane] = d;
   __syncwarp();
-  double acc = x0, mine = x0;
+  double acc = x0;
 #pragma unroll 8
   for (uint32_t j = 0; j < q; j++) {
     acc = acc + ws.dbuf[j];
-    if ((int)j == lane) mine = acc;
+    ws.dbuf[j] = acc;
   }
   __syncwarp();
-  return (uint32_t)lane < q ? mine : acc;
+  const double mine = (uint32_t)lane < q ? ws.dbuf[lane] : acc;
+  __syncwarp();
+  return mine;
 }
 
 // ---- labels with replacement, power-of-two m: PMH1, PMH3, uw3 -------------
