@@ -214,6 +214,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sequential", action="store_true",
+                    help="launch the variants one after another instead of concurrently")
     ap.add_argument("--variants", default=",".join(VARIANTS))
     args = ap.parse_args()
     if args.impl == "reference":
@@ -253,12 +255,38 @@ def main():
                                           off.data_ptr(), S, sig.data_ptr(), None,
                                           status.data_ptr(), sp))
 
+    # one step = the batch sketched by every variant.  Default: all variants
+    # in ONE pmh_sketch_csr_multi_async call (concurrent internal streams, so
+    # each kernel's tail overlaps the others' work); --sequential launches
+    # them one after another on this stream.
+    sigs_multi = [torch.empty((S, M), dtype=torch.int64, device="cuda") for _ in variants]
+    arr_a = (ctypes.c_int * len(variants))(*[_lib.ALG[v] for v in variants])
+    arr_s = (ctypes.c_void_p * len(variants))(*[t.data_ptr() for t in sigs_multi])
+
+    def launch_step():
+        if args.sequential:
+            for v in variants:
+                launch(v)
+        else:
+            _lib.check(L.pmh_sketch_csr_multi_async(arr_a, len(variants), M, ids.data_ptr(),
+                                                    w.data_ptr(), off.data_ptr(), S, arr_s, None,
+                                                    status.data_ptr(), sp))
+
     for _ in range(args.warmup):
+        launch_step()
+    torch.cuda.synchronize()
+    # per-variant device time, each variant alone (outside the timed region)
+    ev = {v: [] for v in variants}
+    for _ in range(2):
         for v in variants:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
             launch(v)
+            b.record(stream)
+            ev[v].append((a, b))
     torch.cuda.synchronize()
 
-    ev = {v: [] for v in variants}
     clk_sampler = ClockSampler(local)
     if world > 1:
         dist.barrier()
@@ -268,13 +296,7 @@ def main():
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
         for _ in range(args.steps):
-            for v in variants:
-                a = torch.cuda.Event(enable_timing=True)
-                b = torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                launch(v)
-                b.record(stream)
-                ev[v].append((a, b))
+            launch_step()
         t_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -370,7 +392,11 @@ def main():
         "dtype": "f64+u64", "data": "synthetic",
         "config": {"workload": "config2: 10k log-uniform weighted sets, 7 weighted variants, m=1024",
                    "sets_per_gpu": S, "elements_per_gpu": N, "m": M,
-                   "variants": variants, "l2": "inputs 1.47 GB > 126 MB L2"},
+                   "variants": variants, "l2": "inputs 1.47 GB > 126 MB L2",
+                   "schedule": ("sequential" if args.sequential else
+                                "concurrent (pmh_sketch_csr_multi_async)")},
+        # each variant timed ALONE (outside the timed region); the step runs
+        # them concurrently, so the step is shorter than their sum
         "per_variant_ms": per_variant_ms,
         "per_variant_elems_per_s": {v: N / (t / 1e3) for v, t in per_variant_ms.items()},
         "e2e": {"value": world * len(variants) * N / e2e_s, "unit": UNIT,

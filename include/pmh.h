@@ -90,6 +90,20 @@ int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
                          const double* weights, const int64_t* offsets,
                          int64_t nsets, uint64_t* sig_out, int64_t* stats_out,
                          int64_t* d_status, void* stream);
+
+/*
+ * The same batch sketched by nalgos algorithms (sig_outs[k] / stats_outs[k]
+ * for algos[k], device buffers; stats_outs or its entries may be NULL):
+ * the variants run CONCURRENTLY on internal streams forked from and joined
+ * back into `stream` (no host sync), so one kernel's tail overlaps the next
+ * one's work.  Each signature equals the single-algorithm call's.  The
+ * reference has no multi-algorithm call; this is the batched form of N calls
+ * of K._k_sketch_dispatch (K:884-917) over the same input.
+ */
+int pmh_sketch_csr_multi_async(const int* algos, int nalgos, int64_t m, const uint64_t* ids,
+                               const double* weights, const int64_t* offsets, int64_t nsets,
+                               uint64_t* const* sig_outs, int64_t* const* stats_outs,
+                               int64_t* d_status, void* stream);
 int pmh_status_reset(int64_t* d_status, void* stream);
 int pmh_status_check(const int64_t* d_status, int64_t* err_set, void* stream);
 

@@ -34,6 +34,7 @@ UNWEIGHTED_IDS = {10, 11, 12, 13, 14, 15, 16, 17, 18}
 
 # every symbol include/pmh.h declares
 EXPORTS = ("pmh_version", "pmh_last_error", "pmh_sketch_csr", "pmh_sketch_csr_async",
+           "pmh_sketch_csr_multi_async",
            "pmh_status_reset", "pmh_status_check", "pmh_sketch_csr_host", "pmh_sketch_csr_host_multi",
            "pmh_count_equal", "pmh_allpairs_tile", "pmh_allpairs_hist", "pmh_bbit",
            "pmh_mse_cell", "pmh_probe_alu_peak")
@@ -69,6 +70,9 @@ def load():
         L.pmh_sketch_csr_async.argtypes = [ctypes.c_int, _i64, _vp, _vp, _vp, _i64, _vp, _vp,
                                            _vp, _vp]
         L.pmh_sketch_csr_async.restype = ctypes.c_int
+        L.pmh_sketch_csr_multi_async.argtypes = [_vp, ctypes.c_int, _i64, _vp, _vp, _vp, _i64,
+                                                 _vp, _vp, _vp, _vp]
+        L.pmh_sketch_csr_multi_async.restype = ctypes.c_int
         L.pmh_status_reset.argtypes = [_vp, _vp]
         L.pmh_status_reset.restype = ctypes.c_int
         L.pmh_status_check.argtypes = [_vp, _i64p, _vp]

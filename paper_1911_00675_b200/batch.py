@@ -88,6 +88,33 @@ def sketch_csr_device(algo, m: int, ids, weights, offsets, want_stats=True):
     return sig, stats
 
 
+def sketch_csr_multi_device(algos, m: int, ids, weights, offsets, want_stats=False):
+    """Device-resident batch sketched by several algorithms concurrently
+    (pmh_sketch_csr_multi_async + one status check) -> list of (sig, stats)."""
+    torch = _torch()
+    aids = [algo_id(a) for a in algos]
+    nsets = offsets.numel() - 1
+    dev = ids.device
+    sigs = [torch.empty((max(nsets, 0), m), dtype=torch.int64, device=dev) for _ in aids]
+    stats = [torch.empty((max(nsets, 0), 3), dtype=torch.int64, device=dev) if want_stats
+             else None for _ in aids]
+    L = _lib.load()
+    sp = _stream_ptr(torch, dev)
+    status = torch.empty(2, dtype=torch.int64, device=dev)
+    _lib.check(L.pmh_status_reset(status.data_ptr(), sp))
+    arr_a = (ctypes.c_int * len(aids))(*aids)
+    arr_s = (ctypes.c_void_p * len(aids))(*[t.data_ptr() for t in sigs])
+    arr_t = (ctypes.c_void_p * len(aids))(*[t.data_ptr() if t is not None else None for t in stats])
+    rc = L.pmh_sketch_csr_multi_async(arr_a, len(aids), m, ids.data_ptr(),
+                                      weights.data_ptr() if weights is not None else None,
+                                      offsets.data_ptr(), nsets, arr_s, arr_t,
+                                      status.data_ptr(), sp)
+    _lib.check(rc)
+    err = ctypes.c_int64(-1)
+    _lib.check(L.pmh_status_check(status.data_ptr(), ctypes.byref(err), sp), err.value)
+    return list(zip(sigs, stats))
+
+
 def sketch_csr(algo, m: int, ids, weights, offsets, want_stats=True):
     """Host-array batch sketch -> (sig uint64[S, m], stats int64[S, 3]).
 

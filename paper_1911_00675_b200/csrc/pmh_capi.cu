@@ -235,13 +235,16 @@ struct AuxStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
-std::map<int, AuxStream> g_aux;
+// keyed by (device, slot): slot 0 serves caller streams, slot k + 1 the k-th
+// internal lane of pmh_sketch_csr_multi_async (so concurrent variants do not
+// serialise their small-set kernels through one stream)
+std::map<std::pair<int, int>, AuxStream> g_aux;
 
-int get_aux(AuxStream** out) {
+int get_aux(AuxStream** out, int slot = 0) {
   int dev = 0;
   PMH_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_mu);
-  auto it = g_aux.find(dev);
+  auto it = g_aux.find({dev, slot});
   if (it == g_aux.end()) {
     AuxStream a;
     // highest priority: the small-set kernel's (few, latency-bound) CTAs are
@@ -254,9 +257,35 @@ int get_aux(AuxStream** out) {
     PMH_CUDA(cudaStreamCreateWithPriority(&a.s, cudaStreamNonBlocking, prio));
     PMH_CUDA(cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming));
     PMH_CUDA(cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming));
-    it = g_aux.emplace(dev, a).first;
+    it = g_aux.emplace(std::make_pair(dev, slot), a).first;
   }
   *out = &it->second;
+  return PMH_OK;
+}
+
+// per-device pool of internal streams for the concurrent multi-variant entry
+struct LanePool {
+  std::vector<cudaStream_t> s;
+  std::vector<cudaEvent_t> done;
+  cudaEvent_t fork = nullptr;
+};
+std::map<int, LanePool> g_lanes;
+
+int get_lanes(int n, LanePool** out) {
+  int dev = 0;
+  PMH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  LanePool& p = g_lanes[dev];
+  if (!p.fork) PMH_CUDA(cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming));
+  while ((int)p.s.size() < n) {
+    cudaStream_t st;
+    cudaEvent_t ev;
+    PMH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    PMH_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    p.s.push_back(st);
+    p.done.push_back(ev);
+  }
+  *out = &p;
   return PMH_OK;
 }
 
@@ -328,11 +357,59 @@ int pmh_status_check(const int64_t* d_status, int64_t* err_set, void* stream) {
   return PMH_OK;
 }
 
+static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const double* weights,
+                             const int64_t* offsets, int64_t nsets, uint64_t* sig_out,
+                             int64_t* stats_out, int64_t* d_status, cudaStream_t st,
+                             int aux_slot);
+
 int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
                          const double* weights, const int64_t* offsets,
                          int64_t nsets, uint64_t* sig_out, int64_t* stats_out,
                          int64_t* d_status, void* stream) {
+  return sketch_async_impl(algo, m, ids, weights, offsets, nsets, sig_out, stats_out, d_status,
+                           (cudaStream_t)stream, 0);
+}
+
+int pmh_sketch_csr_multi_async(const int* algos, int nalgos, int64_t m, const uint64_t* ids,
+                               const double* weights, const int64_t* offsets, int64_t nsets,
+                               uint64_t* const* sig_outs, int64_t* const* stats_outs,
+                               int64_t* d_status, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  if (nalgos < 1 || nalgos > 32 || !algos || !sig_outs)
+    return set_error(PMH_ERR_INVALID, "1..32 algorithms with outputs required");
+  for (int k = 0; k < nalgos; k++) {
+    int vrc = validate_sketch(algos[k], m, weights, nsets);
+    if (vrc != PMH_OK) return vrc;
+  }
+  if (nsets == 0) return PMH_OK;
+  if (!d_status) return set_error(PMH_ERR_INVALID, "status buffer required");
+  LanePool* lp = nullptr;
+  int rc = get_lanes(nalgos, &lp);
+  if (rc) return rc;
+  PMH_CUDA(cudaEventRecord(lp->fork, st));
+  // the P-MinHash-type variants (one long, tail-light kernel) last: their
+  // CTAs fill the tails of the ProbMinHash kernels launched before them
+  std::vector<int> order;
+  for (int pass = 0; pass < 2; pass++)
+    for (int k = 0; k < nalgos; k++) {
+      const bool pmin = algos[k] == ALG_PMINHASH || algos[k] == ALG_MINHASH;
+      if (pmin == (pass == 1)) order.push_back(k);
+    }
+  for (int k : order) {
+    PMH_CUDA(cudaStreamWaitEvent(lp->s[k], lp->fork, 0));
+    rc = sketch_async_impl(algos[k], m, ids, weights, offsets, nsets, sig_outs[k],
+                           stats_outs ? stats_outs[k] : nullptr, d_status, lp->s[k], k + 1);
+    PMH_CUDA(cudaEventRecord(lp->done[k], lp->s[k]));
+    PMH_CUDA(cudaStreamWaitEvent(st, lp->done[k], 0));
+    if (rc != PMH_OK) return rc;
+  }
+  return PMH_OK;
+}
+
+static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const double* weights,
+                             const int64_t* offsets, int64_t nsets, uint64_t* sig_out,
+                             int64_t* stats_out, int64_t* d_status, cudaStream_t st,
+                             int aux_slot) {
   const int fam = family_of(algo);
   int vrc = validate_sketch(algo, m, weights, nsets);
   if (vrc != PMH_OK) return vrc;
@@ -398,7 +475,7 @@ int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
     // small sets run warp-per-set on the auxiliary stream, concurrently with
     // the CTA-per-set kernel on `st` (fork/join with events)
     AuxStream* aux = nullptr;
-    rc = get_aux(&aux);
+    rc = get_aux(&aux, aux_slot);
     if (rc) { cudaFreeAsync(order_ws, st); return rc; }
     PMH_CUDA(cudaEventRecord(aux->fork, st));
     PMH_CUDA(cudaStreamWaitEvent(aux->s, aux->fork, 0));

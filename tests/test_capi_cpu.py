@@ -105,3 +105,17 @@ def test_compute_fails_loudly_without_cuda(monkeypatch):
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         probminhash1(WeightedSet([(1, 1.0)]), 8)
+
+
+def test_multi_async_validates_before_device_work():
+    import ctypes
+    L = _lib.load()
+    arr = (ctypes.c_int * 2)(1, 99)
+    outs = (ctypes.c_void_p * 2)(None, None)
+    rc = L.pmh_sketch_csr_multi_async(arr, 2, 64, None, None, None, 3, outs, None, None, None)
+    assert rc == _lib.PMH_ERR_INVALID
+    rc = L.pmh_sketch_csr_multi_async(arr, 0, 64, None, None, None, 3, outs, None, None, None)
+    assert rc == _lib.PMH_ERR_INVALID
+    one = (ctypes.c_int * 1)(4)
+    rc = L.pmh_sketch_csr_multi_async(one, 1, 1, None, None, None, 3, outs, None, None, None)
+    assert rc == _lib.PMH_ERR_INVALID   # PMH3 needs m >= 2

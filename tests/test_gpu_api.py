@@ -307,3 +307,19 @@ def test_host_multi_matches_single_calls():
     with pytest.raises(EmptyInputError):
         sketch_csr_multi(["probminhash1"], 16, np.arange(3, dtype=np.uint64), np.ones(3),
                          np.array([0, 3, 3]))
+
+
+def test_multi_async_matches_single_calls():
+    """pmh_sketch_csr_multi_async (variants on concurrent internal streams)
+    == the oracle for every algorithm, weighted and unweighted, with stats."""
+    from paper_1911_00675_b200.batch import sketch_csr_multi_device, to_device_f64, to_device_i64, to_device_u64
+    b = datagen.random_sets(33, list(np.exp(np.linspace(0, 9.0, 48)).astype(int) + 1), "pareto1.5")
+    algos = ["probminhash1", "probminhash1a", "probminhash2", "probminhash3", "probminhash3a",
+             "probminhash4", "pminhash", "unweighted3", "unweighted4", "minhash"]
+    outs = sketch_csr_multi_device(algos, 256, to_device_u64(b.ids), to_device_f64(b.weights),
+                                   to_device_i64(b.offsets), want_stats=True)
+    for a, (sg, st) in zip(algos, outs):
+        w = None if a in ("unweighted3", "unweighted4", "minhash") else b.weights
+        ref, _ = orc.sketch_csr(a, 256, b.ids, w, b.offsets, threads=16)
+        assert np.array_equal(sg.cpu().numpy().view(np.uint64), ref), a
+        assert st is not None and (st.cpu().numpy()[:, 0] > 0).all()
