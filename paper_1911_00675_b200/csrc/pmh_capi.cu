@@ -592,16 +592,27 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
     evs.push_back(ev);
     return ev;
   };
-  // offsets + status first, then the element arrays in NC set-chunks on the
-  // copy-in stream; the first algorithm runs chunk by chunk as they land
-  // (CSR offsets are absolute, so a chunk is just offsets + s0)
+  // Schedule (the copy-in is the long pole: 1.39 GB at ~55 GB/s for config 2):
+  //  * offsets + status first, then the element arrays in NC set-chunks on
+  //    the copy-in stream;
+  //  * every ProbMinHash-type algorithm ("chunkable": its per-chunk kernels
+  //    cost about the same as one whole-batch kernel) sketches each chunk as
+  //    soon as it lands, on that chunk's stream, and the chunk's signature
+  //    rows go back on the copy-out stream right away;
+  //  * P-MinHash / MinHash (one long compute-bound kernel that chunking slows
+  //    down) run over the whole batch once every chunk has landed, their
+  //    D2H overlapping whatever still runs.
   e = cudaMemcpyAsync(d_off, offsets, bo, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) rc = cuda_fail(e, "H2D offsets");
   if (rc == PMH_OK) rc = pmh_status_reset(d_status, st);
   cudaEvent_t ev_meta = mkev();
   cudaEventRecord(ev_meta, st);
   cudaStreamWaitEvent(cin, ev_meta, 0);
-  const int NC = nsets >= 8 && nelems >= (1 << 20) ? 4 : 1;
+  int NC = nsets >= 8 && nelems >= (1 << 20) ? 4 : 1;
+  if (const char* ev = getenv("PMH_H2D_CHUNKS")) {
+    const int v = atoi(ev);
+    if (v >= 1 && v <= 8 && nsets >= v) NC = v;
+  }
   std::vector<int64_t> cut(NC + 1, 0);
   cut[NC] = nsets;
   for (int c = 1; c < NC; c++) {  // element-balanced set boundaries
@@ -610,9 +621,9 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
     while (lo < hi) { const int64_t mid = (lo + hi) / 2; if (offsets[mid] < target) lo = mid + 1; else hi = mid; }
     cut[c] = lo;
   }
-  // each chunk of the first algorithm runs on its own stream so the chunks'
-  // LPT tails overlap (one stream would serialise four tails)
-  cudaStream_t cst[4] = {nullptr, nullptr, nullptr, nullptr};
+  auto chunkable = [&](int k) { return algos[k] != ALG_PMINHASH && algos[k] != ALG_MINHASH; };
+  std::vector<cudaEvent_t> chunk_done;
+  cudaStream_t cst[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   for (int c = 0; c < NC; c++) cudaStreamCreateWithFlags(&cst[c], cudaStreamNonBlocking);
   for (int c = 0; c < NC && rc == PMH_OK; c++) {
     const int64_t e0 = offsets[cut[c]], e1 = offsets[cut[c + 1]];
@@ -629,24 +640,42 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
     cudaEventRecord(ev, cin);
     cudaStreamWaitEvent(cst[c], ev, 0);
     const int64_t ns = cut[c + 1] - cut[c];
-    if (ns > 0) {
-      uint64_t* sig0 = (uint64_t*)d_out + (size_t)cut[c] * m;
-      int64_t* st0 = want_stats ? (int64_t*)(d_out + bs) + 3 * cut[c] : nullptr;
-      rc = pmh_sketch_csr_async(algos[0], m, d_ids, weighted ? d_w : nullptr, d_off + cut[c], ns,
+    for (int k = 0; k < nalgos && rc == PMH_OK && ns > 0; k++) {
+      if (!chunkable(k)) continue;
+      char* outk = d_out + per_algo * (size_t)k;
+      uint64_t* sig0 = (uint64_t*)outk + (size_t)cut[c] * m;
+      int64_t* st0 = want_stats ? (int64_t*)(outk + bs) + 3 * cut[c] : nullptr;
+      rc = pmh_sketch_csr_async(algos[k], m, d_ids, weighted ? d_w : nullptr, d_off + cut[c], ns,
                                 sig0, st0, d_status, cst[c]);
+      if (rc != PMH_OK) break;
+      cudaEvent_t evk = mkev();
+      cudaEventRecord(evk, cst[c]);
+      cudaStreamWaitEvent(cout, evk, 0);
+      const size_t rows = (size_t)ns * (size_t)m * sizeof(uint64_t);
+      if ((e = cudaMemcpyAsync(sig_outs[k] + (size_t)cut[c] * m, sig0, rows, cudaMemcpyDeviceToHost,
+                               cout)) != cudaSuccess ||
+          (want_stats && stats_outs[k] &&
+           (e = cudaMemcpyAsync(stats_outs[k] + 3 * cut[c], st0, sizeof(int64_t) * 3 * (size_t)ns,
+                                cudaMemcpyDeviceToHost, cout)) != cudaSuccess)) {
+        rc = cuda_fail(e, "D2H");
+        break;
+      }
     }
     cudaEvent_t evc = mkev();
     cudaEventRecord(evc, cst[c]);
-    cudaStreamWaitEvent(st, evc, 0);
+    chunk_done.push_back(evc);
   }
-  // remaining algorithms over the whole batch; each result's D2H overlaps the
-  // next algorithm's compute on the copy-out stream
+  // whole-batch algorithms as soon as every chunk is resident (they overlap
+  // the chunk streams' remaining work)
+  cudaEvent_t ev_in = mkev();
+  cudaEventRecord(ev_in, cin);
+  cudaStreamWaitEvent(st, ev_in, 0);
   for (int k = 0; k < nalgos && rc == PMH_OK; k++) {
+    if (chunkable(k)) continue;
     char* outk = d_out + per_algo * (size_t)k;
-    if (k > 0)
-      rc = pmh_sketch_csr_async(algos[k], m, d_ids, weighted ? d_w : nullptr, d_off, nsets,
-                                (uint64_t*)outk, want_stats ? (int64_t*)(outk + bs) : nullptr,
-                                d_status, st);
+    rc = pmh_sketch_csr_async(algos[k], m, d_ids, weighted ? d_w : nullptr, d_off, nsets,
+                              (uint64_t*)outk, want_stats ? (int64_t*)(outk + bs) : nullptr,
+                              d_status, st);
     if (rc != PMH_OK) break;
     cudaEvent_t ev = mkev();
     cudaEventRecord(ev, st);
@@ -658,6 +687,7 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
       break;
     }
   }
+  for (cudaEvent_t evc : chunk_done) cudaStreamWaitEvent(st, evc, 0);
   cudaEvent_t ev_end = mkev();
   cudaEventRecord(ev_end, cout);
   cudaStreamWaitEvent(st, ev_end, 0);
