@@ -157,6 +157,24 @@ int pmh_bbit(const uint64_t* sig, int64_t nsets, int64_t m, int b,
              int64_t* out, void* stream);
 
 /*
+ * Packed b-bit signatures (the "popc-style" estimator of SURVEY §8f-1):
+ * pmh_bbit_pack fuses the b-bit reduction (estimate.py:105-114, K:851-861)
+ * with packing -- row s, word w holds components k = w*F + f (F = floor(64/b),
+ * f < F) at bits [f*b, f*b + b), unused fields 0; pmh_bbit_words(m, b) =
+ * ceil(m / F) words per row (-1 on bad arguments).
+ * pmh_allpairs_bbit_hist is pmh_allpairs_hist over packed rows: hist[C] counts
+ * the pairs (j > i) with C equal b-bit components; pairs with C >= thr are
+ * appended.  The estimate of a pair is clamp((C/m - 2^-b)/(1 - 2^-b), 0, 1)
+ * (estimate_similarity_bbit, estimate.py:117-123).
+ */
+int64_t pmh_bbit_words(int64_t m, int b);
+int pmh_bbit_pack(const uint64_t* sig, int64_t nsets, int64_t m, int b, uint64_t* packed,
+                  void* stream);
+int pmh_allpairs_bbit_hist(const uint64_t* packed, int64_t n, int64_t m, int b, int64_t r0,
+                           int64_t r1, int64_t c0, int64_t c1, int32_t thr, uint64_t* hist,
+                           uint64_t* pairs, int64_t cap, uint64_t* cursor, void* stream);
+
+/*
  * Fused MSE cell: replaces K._k_mse_cell(algo, m, wa, wb, seed, s) (K:920-963,
  * called by harness.run_mse_cell harness.py:266-280).  For each of s pairs
  * the ids come from ONE splitmix64 stream seeded with `seed` (pair t, weight

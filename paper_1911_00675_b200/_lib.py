@@ -37,6 +37,7 @@ EXPORTS = ("pmh_version", "pmh_last_error", "pmh_sketch_csr", "pmh_sketch_csr_as
            "pmh_sketch_csr_multi_async",
            "pmh_status_reset", "pmh_status_check", "pmh_sketch_csr_host", "pmh_sketch_csr_host_multi",
            "pmh_count_equal", "pmh_allpairs_tile", "pmh_allpairs_hist", "pmh_bbit",
+           "pmh_bbit_words", "pmh_bbit_pack", "pmh_allpairs_bbit_hist",
            "pmh_mse_cell", "pmh_probe_alu_peak")
 
 _lib = None
@@ -93,6 +94,13 @@ def load():
         L.pmh_allpairs_hist.restype = ctypes.c_int
         L.pmh_bbit.argtypes = [_vp, _i64, _i64, ctypes.c_int, _vp, _vp]
         L.pmh_bbit.restype = ctypes.c_int
+        L.pmh_bbit_words.argtypes = [_i64, ctypes.c_int]
+        L.pmh_bbit_words.restype = _i64
+        L.pmh_bbit_pack.argtypes = [_vp, _i64, _i64, ctypes.c_int, _vp, _vp]
+        L.pmh_bbit_pack.restype = ctypes.c_int
+        L.pmh_allpairs_bbit_hist.argtypes = [_vp, _i64, _i64, ctypes.c_int, _i64, _i64, _i64, _i64,
+                                             ctypes.c_int32, _vp, _vp, _i64, _vp, _vp]
+        L.pmh_allpairs_bbit_hist.restype = ctypes.c_int
         L.pmh_mse_cell.argtypes = [ctypes.c_int, _i64, _vp, _vp, _i64, ctypes.c_uint64, _i64,
                                    _vp, _vp]
         L.pmh_mse_cell.restype = ctypes.c_int

@@ -211,11 +211,7 @@ def allpairs_hist_device(sigs, r0=0, r1=None, c0=0, c1=None, threshold=1, cap=1 
                                        cursor.data_ptr(), _stream_ptr(torch, sigs.device))
     _lib.check(rc)
     k = int(cursor.item())
-    got = pairs[: min(k, cap)].cpu().numpy()
-    ij = got[:, 0].view(np.uint64)
-    out = np.stack([(ij >> np.uint64(32)).astype(np.int64),
-                    (ij & np.uint64(0xFFFFFFFF)).astype(np.int64), got[:, 1]], axis=1)
-    return hist, out, k
+    return hist, _pairs_out(pairs, k, cap), k
 
 
 def bbit_device(sig, b: int):
@@ -226,6 +222,72 @@ def bbit_device(sig, b: int):
                               _stream_ptr(torch, sig.device))
     _lib.check(rc)
     return out
+
+
+def _pairs_out(pairs, k, cap):
+    got = pairs[: min(k, cap)].cpu().numpy()
+    ij = got[:, 0].view(np.uint64)
+    return np.stack([(ij >> np.uint64(32)).astype(np.int64),
+                     (ij & np.uint64(0xFFFFFFFF)).astype(np.int64), got[:, 1]], axis=1)
+
+
+def bbit_words(m: int, b: int) -> int:
+    """Packed words per row: floor(64/b) b-bit fields per word."""
+    return -(-m // (64 // b))
+
+
+def bbit_pack_device(sig, b: int):
+    """Fused b-bit reduction (estimate.py:105-114, K:851-861) + packing of a
+    [S, m] signature batch -> int64 [S, bbit_words(m, b)] CUDA tensor."""
+    torch = _torch()
+    S, m = sig.shape
+    if not 1 <= b <= 16:
+        raise InvalidParamsError("b must be in 1..16")
+    out = torch.empty((S, bbit_words(m, b)), dtype=torch.int64, device=sig.device)
+    rc = _lib.load().pmh_bbit_pack(sig.contiguous().data_ptr(), S, m, b, out.data_ptr(),
+                                   _stream_ptr(torch, sig.device))
+    _lib.check(rc)
+    return out
+
+
+def bbit_unpack(packed: np.ndarray, m: int, b: int) -> np.ndarray:
+    """Host helper: packed words -> int64 [S, m] b-bit components."""
+    fpw = 64 // b
+    p = np.ascontiguousarray(packed).view(np.uint64)
+    k = np.arange(m)
+    words = p[:, k // fpw]
+    return ((words >> (np.uint64(b) * (k % fpw).astype(np.uint64))) &
+            np.uint64((1 << b) - 1)).astype(np.int64)
+
+
+def allpairs_bbit_hist_device(packed, m: int, b: int, r0=0, r1=None, c0=0, c1=None,
+                              threshold=1, cap=1 << 22, hist=None):
+    """As allpairs_hist_device for packed b-bit rows (bbit_pack_device):
+    histogram of equal b-bit component counts C (int64 [m+1]) and the pairs
+    with C >= threshold.  The collision-corrected estimate of a pair is
+    bbit_estimate(C, m, b) (estimate.py:117-123)."""
+    torch = _torch()
+    n = packed.shape[0]
+    r1 = n if r1 is None else r1
+    c1 = n if c1 is None else c1
+    if hist is None:
+        hist = torch.zeros(m + 1, dtype=torch.int64, device=packed.device)
+    pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=packed.device)
+    cursor = torch.zeros(1, dtype=torch.int64, device=packed.device)
+    rc = _lib.load().pmh_allpairs_bbit_hist(packed.contiguous().data_ptr(), n, m, b, r0, r1, c0,
+                                            c1, int(threshold), hist.data_ptr(), pairs.data_ptr(),
+                                            cap, cursor.data_ptr(), _stream_ptr(torch, packed.device))
+    _lib.check(rc)
+    k = int(cursor.item())
+    return hist, _pairs_out(pairs, k, cap), k
+
+
+def bbit_estimate(count, m: int, b: int):
+    """(C/m - 2^-b) / (1 - 2^-b) clamped to [0, 1] (estimate.py:117-123),
+    vectorised over equal-component counts C."""
+    c = np.asarray(count, np.float64) / m
+    p = 2.0 ** -b
+    return np.minimum(1.0, np.maximum(0.0, (c - p) / (1.0 - p)))
 
 
 def sigs_to_numpy(sig) -> np.ndarray:

@@ -737,30 +737,89 @@ int pmh_allpairs_tile(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0,
   return PMH_OK;
 }
 
+}  // extern "C"
+
+namespace {
+template <class Cmp>
+int launch_allpairs_reduce(const uint64_t* rows, int64_t len, int64_t m, Cmp cmp, int64_t r0,
+                           int64_t r1, int64_t c0, int64_t c1, int32_t thr, uint64_t* hist,
+                           uint64_t* pairs, int64_t cap, uint64_t* cursor, cudaStream_t st) {
+  const size_t smem = 2 * sizeof(uint64_t) * AP_KS * (AP_TILE + 1) + sizeof(unsigned) * (size_t)(m + 1);
+  PMH_CUDA(cudaFuncSetAttribute(allpairs_reduce_kernel<Cmp>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, allpairs_reduce_kernel<Cmp>, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ntiles = ((r1 - r0 + AP_TILE - 1) / AP_TILE) * ((c1 - c0 + AP_TILE - 1) / AP_TILE);
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > ntiles) grid = ntiles;
+  allpairs_reduce_kernel<Cmp><<<(unsigned)grid, 256, smem, st>>>(
+      rows, len, m, cmp, r0, r1, c0, c1, thr, (unsigned long long*)hist,
+      (unsigned long long*)pairs, cap, (unsigned long long*)cursor);
+  PMH_CUDA(cudaGetLastError());
+  return PMH_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int pmh_allpairs_hist(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0, int64_t r1,
                       int64_t c0, int64_t c1, int32_t thr, uint64_t* hist, uint64_t* pairs,
                       int64_t cap, uint64_t* cursor, void* stream) {
   if (m < 1 || m > 65535 || r0 < 0 || r1 > n || c0 < 0 || c1 > n || r0 > r1 || c0 > c1)
     return set_error(PMH_ERR_INVALID, "bad tile bounds");
   if (r0 == r1 || c0 == c1) return PMH_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  const size_t smem = 2 * sizeof(uint64_t) * AP_KS * (AP_TILE + 1) + sizeof(unsigned) * (size_t)(m + 1);
-  PMH_CUDA(cudaFuncSetAttribute(allpairs_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, allpairs_hist_kernel, 256, smem);
-  if (per_sm < 1) per_sm = 1;
-  const int64_t ntiles = ((r1 - r0 + AP_TILE - 1) / AP_TILE) * ((c1 - c0 + AP_TILE - 1) / AP_TILE);
-  int64_t grid = (int64_t)sms * per_sm;
-  if (grid > ntiles) grid = ntiles;
-  allpairs_hist_kernel<<<(unsigned)grid, 256, smem, st>>>(
-      sigs, m, r0, r1, c0, c1, thr, (unsigned long long*)hist, (unsigned long long*)pairs, cap,
-      (unsigned long long*)cursor);
+  return launch_allpairs_reduce(sigs, m, m, EqU64{}, r0, r1, c0, c1, thr, hist, pairs, cap,
+                                cursor, (cudaStream_t)stream);
+}
+
+int64_t pmh_bbit_words(int64_t m, int b) {
+  if (m < 1 || b < 1 || b > 16) return -1;
+  const int64_t fpw = 64 / b;
+  return (m + fpw - 1) / fpw;
+}
+
+int pmh_bbit_pack(const uint64_t* sig, int64_t nsets, int64_t m, int b, uint64_t* packed,
+                  void* stream) {
+  if (b < 1 || b > 16) return set_error(PMH_ERR_INVALID, "b must be in 1..16");
+  if (m < 1 || nsets < 0) return set_error(PMH_ERR_INVALID, "bad sizes");
+  const int64_t W = pmh_bbit_words(m, b);
+  const int64_t total = nsets * W;
+  if (total == 0) return PMH_OK;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  bbit_pack_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(sig, nsets, m, b, 64 / b,
+                                                                       W, packed);
   PMH_CUDA(cudaGetLastError());
   return PMH_OK;
+}
+
+int pmh_allpairs_bbit_hist(const uint64_t* packed, int64_t n, int64_t m, int b, int64_t r0,
+                           int64_t r1, int64_t c0, int64_t c1, int32_t thr, uint64_t* hist,
+                           uint64_t* pairs, int64_t cap, uint64_t* cursor, void* stream) {
+  if (b < 1 || b > 16) return set_error(PMH_ERR_INVALID, "b must be in 1..16");
+  if (m < 1 || m > 65535 || r0 < 0 || r1 > n || c0 < 0 || c1 > n || r0 > r1 || c0 > c1)
+    return set_error(PMH_ERR_INVALID, "bad tile bounds");
+  if (r0 == r1 || c0 == c1) return PMH_OK;
+  const int fpw = 64 / b;
+  uint64_t H = 0, L = 0;
+  for (int f = 0; f < fpw; f++) {
+    H |= 1ULL << (f * b + b - 1);
+    L |= ((1ULL << (b - 1)) - 1ULL) << (f * b);
+  }
+  const int64_t W = pmh_bbit_words(m, b);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (b) {
+    case 1: return launch_allpairs_reduce(packed, W, m, BBitNeqT<1>{m}, r0, r1, c0, c1, thr, hist, pairs, cap, cursor, st);
+    case 2: return launch_allpairs_reduce(packed, W, m, BBitNeqT<2>{m}, r0, r1, c0, c1, thr, hist, pairs, cap, cursor, st);
+    case 4: return launch_allpairs_reduce(packed, W, m, BBitNeqT<4>{m}, r0, r1, c0, c1, thr, hist, pairs, cap, cursor, st);
+    case 8: return launch_allpairs_reduce(packed, W, m, BBitNeqT<8>{m}, r0, r1, c0, c1, thr, hist, pairs, cap, cursor, st);
+    case 16: return launch_allpairs_reduce(packed, W, m, BBitNeqT<16>{m}, r0, r1, c0, c1, thr, hist, pairs, cap, cursor, st);
+    default: return launch_allpairs_reduce(packed, W, m, BBitNeq{L, H, m}, r0, r1, c0, c1, thr, hist, pairs, cap, cursor, st);
+  }
 }
 
 int pmh_bbit(const uint64_t* sig, int64_t nsets, int64_t m, int b, int64_t* out,

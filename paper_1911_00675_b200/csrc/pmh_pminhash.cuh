@@ -545,9 +545,62 @@ __global__ void __launch_bounds__(256) allpairs_tile_kernel(
 // to `hist`, m+1 bins) and, for count >= thr, the pair appended to `pairs`
 // as (i << 32 | j, count) through a global cursor (dropped beyond `cap`; the
 // cursor still counts them).  No dense count matrix is materialised.
-__global__ void __launch_bounds__(256) allpairs_hist_kernel(
-    const uint64_t* __restrict__ sigs, int64_t m, int64_t r0, int64_t r1, int64_t c0,
-    int64_t c1, int32_t thr, unsigned long long* __restrict__ hist,
+// Comparison policies for the all-pairs reduction.  EqU64: rows of m full
+// signature components, count = number of equal components.  BBitNeq: rows
+// of W packed b-bit words (bbit_pack_kernel), per word the number of UNEQUAL
+// b-bit fields by a carry-free SWAR test -- t = (x & L) + L sets each field's
+// top bit iff its low b-1 bits are nonzero (L = low b-1 bits of every field,
+// H = top bit of every field), nz = (t | x) & H -- so count = m - sum popc.
+// Padding fields are zero in both rows and never counted as unequal.
+struct EqU64 {
+  __device__ __forceinline__ uint32_t op(uint64_t a, uint64_t b) const { return a == b; }
+  __device__ __forceinline__ int64_t finish(uint32_t c) const { return c; }
+};
+struct BBitNeq {
+  uint64_t L, H;
+  int64_t m;
+  __device__ __forceinline__ uint32_t op(uint64_t a, uint64_t b) const {
+    const uint64_t x = a ^ b;
+    return (uint32_t)__popcll((((x & L) + L) | x) & H);
+  }
+  __device__ __forceinline__ int64_t finish(uint32_t c) const { return m - (int64_t)c; }
+};
+// compile-time masks for the common b (the b = 1 case reduces to popc(a ^ b))
+template <int B>
+struct BBitNeqT {
+  int64_t m;
+  __host__ __device__ static constexpr uint64_t mask_h() {
+    uint64_t h = 0;
+    for (int f = 0; f < 64 / B; f++) h |= 1ULL << (f * B + B - 1);
+    return h;
+  }
+  __host__ __device__ static constexpr uint64_t mask_l() {
+    uint64_t l = 0;
+    for (int f = 0; f < 64 / B; f++) l |= ((1ULL << (B - 1)) - 1ULL) << (f * B);
+    return l;
+  }
+  __device__ __forceinline__ uint32_t op(uint64_t a, uint64_t b) const {
+    const uint64_t x = a ^ b;
+    if constexpr (B == 1) {
+      return (uint32_t)__popcll(x);
+    } else {
+      constexpr uint64_t L = mask_l(), H = mask_h();
+      return (uint32_t)__popcll((((x & L) + L) | x) & H);
+    }
+  }
+  __device__ __forceinline__ int64_t finish(uint32_t c) const { return m - (int64_t)c; }
+};
+
+// Tiled all-pairs reduction over rows of `len` words (len = m for EqU64, W
+// for BBitNeq): 64x64 pair tiles, words staged through shared memory in
+// slices of 32, counts reduced on the fly into a per-CTA histogram (m+1
+// bins, flushed once) and the pairs with count >= thr appended as
+// (i << 32 | j, count) through a global cursor (dropped beyond `cap`; the
+// cursor still counts them).  No dense count matrix is materialised.
+template <class Cmp>
+__global__ void __launch_bounds__(256) allpairs_reduce_kernel(
+    const uint64_t* __restrict__ sigs, int64_t len, int64_t m, Cmp cmp, int64_t r0, int64_t r1,
+    int64_t c0, int64_t c1, int32_t thr, unsigned long long* __restrict__ hist,
     unsigned long long* __restrict__ pairs, int64_t cap, unsigned long long* __restrict__ cursor) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t (*sa)[AP_TILE + 1] = reinterpret_cast<uint64_t (*)[AP_TILE + 1]>(smem);
@@ -562,22 +615,25 @@ __global__ void __launch_bounds__(256) allpairs_hist_kernel(
   for (int64_t t = blockIdx.x; t < nti * ntj; t += gridDim.x) {
     const int64_t ti = r0 + (t / ntj) * AP_TILE, tj = c0 + (t % ntj) * AP_TILE;
     if (tj + AP_TILE <= ti + 1) continue;  // entirely on/below the diagonal
-    int cnt[4][4];
+    uint32_t cnt[4][4];
 #pragma unroll
     for (int u = 0; u < 4; u++)
 #pragma unroll
       for (int v = 0; v < 4; v++) cnt[u][v] = 0;
-    for (int64_t k0 = 0; k0 < m; k0 += AP_KS) {
+    for (int64_t k0 = 0; k0 < len; k0 += AP_KS) {
       __syncthreads();
       for (int q = threadIdx.x; q < AP_KS * AP_TILE; q += blockDim.x) {
         const int r = q / AP_KS, kk = q % AP_KS;
         const int64_t gi = ti + r, gj = tj + r, k = k0 + kk;
-        sa[kk][r] = (gi < r1 && k < m) ? __ldg(&sigs[gi * m + k]) : 0x1ULL;
-        sb[kk][r] = (gj < c1 && k < m) ? __ldg(&sigs[gj * m + k]) : 0x2ULL;
+        // out-of-range words: equal in both operands for every policy, the
+        // results of out-of-range rows are discarded
+        sa[kk][r] = (gi < r1 && k < len) ? __ldg(&sigs[gi * len + k]) : 0ULL;
+        sb[kk][r] = (gj < c1 && k < len) ? __ldg(&sigs[gj * len + k]) : 0ULL;
       }
       __syncthreads();
+      const int kn = len - k0 < AP_KS ? (int)(len - k0) : AP_KS;
 #pragma unroll 4
-      for (int kk = 0; kk < AP_KS; kk++) {
+      for (int kk = 0; kk < kn; kk++) {
         uint64_t av[4], bv[4];
 #pragma unroll
         for (int u = 0; u < 4; u++) av[u] = sa[kk][ty * 4 + u];
@@ -586,7 +642,7 @@ __global__ void __launch_bounds__(256) allpairs_hist_kernel(
 #pragma unroll
         for (int u = 0; u < 4; u++)
 #pragma unroll
-          for (int v = 0; v < 4; v++) cnt[u][v] += (av[u] == bv[v]);
+          for (int v = 0; v < 4; v++) cnt[u][v] += cmp.op(av[u], bv[v]);
       }
     }
 #pragma unroll
@@ -596,12 +652,13 @@ __global__ void __launch_bounds__(256) allpairs_hist_kernel(
       for (int v = 0; v < 4; v++) {
         const int64_t j = tj + tx * 4 + v;
         if (i < r1 && j < c1 && j > i) {
-          atomicAdd(&shist[cnt[u][v]], 1u);
-          if (cnt[u][v] >= thr) {
+          const int64_t c = cmp.finish(cnt[u][v]);
+          atomicAdd(&shist[c], 1u);
+          if (c >= thr) {
             const unsigned long long pos = atomicAdd(cursor, 1ULL);
             if ((int64_t)pos < cap) {
               pairs[2 * pos] = ((unsigned long long)i << 32) | (unsigned long long)j;
-              pairs[2 * pos + 1] = (unsigned long long)cnt[u][v];
+              pairs[2 * pos + 1] = (unsigned long long)c;
             }
           }
         }
@@ -611,6 +668,27 @@ __global__ void __launch_bounds__(256) allpairs_hist_kernel(
   __syncthreads();
   for (int64_t b = threadIdx.x; b <= m; b += blockDim.x)
     if (shist[b]) atomicAdd(&hist[b], (unsigned long long)shist[b]);
+}
+
+// Fused b-bit reduction + packing (K:851-861 + layout): word w of row s holds
+// fields k = w * fpw + f (f < fpw = floor(64 / b)) at bits [f b, f b + b),
+// field k = low b bits of mix64(sig_k + GOLDEN (k + 1)); unused fields are 0.
+__global__ void bbit_pack_kernel(const uint64_t* __restrict__ sig, int64_t nsets, int64_t m,
+                                 int b, int fpw, int64_t W, uint64_t* __restrict__ packed) {
+  const uint64_t mask = (1ULL << (uint64_t)b) - 1ULL;
+  const int64_t total = nsets * W;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = q / W, wi = q - s * W;
+    uint64_t word = 0;
+    for (int f = 0; f < fpw; f++) {
+      const int64_t k = wi * fpw + f;
+      if (k >= m) break;
+      const uint64_t h = mix64(sig[s * m + k] + GOLDEN * (uint64_t)(k + 1)) & mask;
+      word |= h << (f * b);
+    }
+    packed[q] = word;
+  }
 }
 
 // b-bit reduction (K:851-861): component i -> low b bits of

@@ -15,7 +15,7 @@ ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 
 def _header_symbols():
     src = open(os.path.join(ROOT, "include", "pmh.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(pmh_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(pmh_\w+)\s*\(", src, re.M)))
 
 
 def test_library_loads_and_exports_header_symbols():
@@ -119,3 +119,31 @@ def test_multi_async_validates_before_device_work():
     one = (ctypes.c_int * 1)(4)
     rc = L.pmh_sketch_csr_multi_async(one, 1, 1, None, None, None, 3, outs, None, None, None)
     assert rc == _lib.PMH_ERR_INVALID   # PMH3 needs m >= 2
+
+
+def test_bbit_words_and_validation():
+    L = _lib.load()
+    for m, b in [(256, 1), (256, 3), (100, 7), (1024, 16), (1, 13)]:
+        assert L.pmh_bbit_words(m, b) == -(-m // (64 // b))
+    assert L.pmh_bbit_words(0, 4) == -1 and L.pmh_bbit_words(8, 17) == -1
+    assert L.pmh_bbit_pack(None, 1, 8, 0, None, None) == _lib.PMH_ERR_INVALID
+    assert L.pmh_allpairs_bbit_hist(None, 4, 8, 17, 0, 4, 0, 4, 1, None, None, 0, None,
+                                    None) == _lib.PMH_ERR_INVALID
+    assert L.pmh_allpairs_bbit_hist(None, 4, 8, 4, 0, 5, 0, 4, 1, None, None, 0, None,
+                                    None) == _lib.PMH_ERR_INVALID
+
+
+def test_bbit_host_helpers():
+    from paper_1911_00675_b200.batch import bbit_estimate, bbit_unpack
+    b, m = 3, 50
+    rng = np.random.default_rng(0)
+    comp = rng.integers(0, 1 << b, size=(4, m))
+    fpw = 64 // b
+    words = np.zeros((4, -(-m // fpw)), np.uint64)
+    for k in range(m):
+        words[:, k // fpw] |= comp[:, k].astype(np.uint64) << np.uint64(b * (k % fpw))
+    assert np.array_equal(bbit_unpack(words.view(np.int64), m, b), comp)
+    # estimate.py:117-123 on a few counts
+    for c in (0, 10, 25, 50):
+        p = 2.0 ** -b
+        assert bbit_estimate(c, m, b) == min(1.0, max(0.0, (c / m - p) / (1 - p)))
