@@ -189,6 +189,18 @@ int pmh_mse_cell(int algo, int64_t m, const double* wa, const double* wb, int64_
                  uint64_t seed, int64_t s, int64_t* matches, void* stream);
 
 /*
+ * Host ingestion of the reference CLI's "id weight" lines
+ * (cli._read_weighted_lines, cli.py:60-70) into CSR arrays, no device work:
+ * blank and '#' lines skipped, id = Python int(tok, 0) (non-negative, < 2^64),
+ * weight = Python float(tok) or 1.0 when absent.  Returns the number of
+ * entries, -(line number) of the first line outside that grammar (the caller
+ * then falls back to the exact restatement for the reference's error),
+ * -(2^62) if more than cap entries, -(2^61) on bad arguments.
+ */
+int64_t pmh_parse_weighted_text(const char* buf, int64_t len, uint64_t* ids, double* weights,
+                                int64_t cap);
+
+/*
  * Diagnostic: measured 32-bit ALU-pipe peak of the current device in Gop/s
  * (8 independent LOP3 chains per thread, full occupancy) -- the roofline
  * denominator for the integer-bound signature kernels.  Synchronous.

@@ -38,7 +38,7 @@ EXPORTS = ("pmh_version", "pmh_last_error", "pmh_sketch_csr", "pmh_sketch_csr_as
            "pmh_status_reset", "pmh_status_check", "pmh_sketch_csr_host", "pmh_sketch_csr_host_multi",
            "pmh_count_equal", "pmh_allpairs_tile", "pmh_allpairs_hist", "pmh_bbit",
            "pmh_bbit_words", "pmh_bbit_pack", "pmh_allpairs_bbit_hist",
-           "pmh_mse_cell", "pmh_probe_alu_peak")
+           "pmh_mse_cell", "pmh_parse_weighted_text", "pmh_probe_alu_peak")
 
 _lib = None
 _lock = threading.Lock()
@@ -101,6 +101,8 @@ def load():
         L.pmh_allpairs_bbit_hist.argtypes = [_vp, _i64, _i64, ctypes.c_int, _i64, _i64, _i64, _i64,
                                              ctypes.c_int32, _vp, _vp, _i64, _vp, _vp]
         L.pmh_allpairs_bbit_hist.restype = ctypes.c_int
+        L.pmh_parse_weighted_text.argtypes = [ctypes.c_char_p, _i64, _vp, _vp, _i64]
+        L.pmh_parse_weighted_text.restype = _i64
         L.pmh_mse_cell.argtypes = [ctypes.c_int, _i64, _vp, _vp, _i64, ctypes.c_uint64, _i64,
                                    _vp, _vp]
         L.pmh_mse_cell.restype = ctypes.c_int

@@ -24,6 +24,7 @@
 #include "pmh_probe.cuh"
 #include "pmh_baselines.cuh"
 #include "pmh_harness.cuh"
+#include "pmh_ingest.h"
 
 using namespace pmh;
 
@@ -922,6 +923,12 @@ int pmh_mse_cell(int algo, int64_t m, const double* wa, const double* wb, int64_
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, st);
   return rc;
+}
+
+int64_t pmh_parse_weighted_text(const char* buf, int64_t len, uint64_t* ids, double* weights,
+                                int64_t cap) {
+  if (!buf || len < 0 || cap < 0 || (cap > 0 && (!ids || !weights))) return -(int64_t(1) << 61);
+  return pmh_ingest::parse_weighted_text(buf, len, ids, weights, cap);
 }
 
 int pmh_probe_alu_peak(double* gops_out, double* ms_out) {

@@ -221,9 +221,29 @@ def main_mse():
     save("mse", **arrays)
 
 
+INGEST_TEXT = (
+    "# header comment\n\n17 0.5\n0x1F 2\n  0o17\t3e-3 trailing tokens\n0b101 inf\n"
+    "1_000_000 1_0.25\n+42 .5\n0X_ff 7.\n18446744073709551615 1e308\n00 1\n"
+    "   # indented comment\n9 -2.5\n10 nan\n0_0 2\n")
+
+
+def main_ingest():
+    # 7) CLI text ingestion (cli._read_weighted_lines, cli.py:60-70)
+    from probminhash import cli
+    import io
+    entries = cli._read_weighted_lines(io.StringIO(INGEST_TEXT))
+    save("ingest", text=np.array(INGEST_TEXT),
+         ids=np.array([e for e, _ in entries], np.uint64),
+         weights=np.array([w for _, w in entries], np.float64))
+
+
 if __name__ == "__main__":
-    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "mse":
+    only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
+    if only == "mse":
         main_mse()
+    elif only == "ingest":
+        main_ingest()
     else:
         main()
         main_mse()
+        main_ingest()

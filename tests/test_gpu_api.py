@@ -323,3 +323,25 @@ def test_multi_async_matches_single_calls():
         ref, _ = orc.sketch_csr(a, 256, b.ids, w, b.offsets, threads=16)
         assert np.array_equal(sg.cpu().numpy().view(np.uint64), ref), a
         assert st is not None and (st.cpu().numpy()[:, 0] > 0).all()
+
+
+def test_text_ingestion_to_signatures(tmp_path):
+    """CLI-format text files -> CSR (native parser) -> GPU sketch == oracle."""
+    from paper_1911_00675_b200.ingest import read_sets_csr
+    rng = np.random.default_rng(8)
+    srcs = []
+    for s in range(6):
+        n = int(rng.integers(1, 400))
+        ids = rng.choice(2**40, size=n, replace=False)
+        w = rng.exponential(size=n) + 1e-3
+        lines = ["# set %d" % s] + [f"{hex(int(i)) if k % 3 == 0 else int(i)} {float(x)!r}"
+                                    for k, (i, x) in enumerate(zip(ids, w))]
+        p = tmp_path / f"s{s}.txt"
+        p.write_text("\n".join(lines) + "\n")
+        srcs.append(str(p))
+    b = read_sets_csr(srcs)
+    for algo in ("probminhash4", "pminhash"):
+        sig, _ = sketch_batch(algo, to_device_u64(b.ids), to_device_f64(b.weights),
+                              to_device_i64(b.offsets), 128)
+        ref, _ = orc.sketch_csr(algo, 128, b.ids, b.weights, b.offsets)
+        assert np.array_equal(sig.cpu().numpy().view(np.uint64), ref)

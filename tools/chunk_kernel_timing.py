@@ -18,9 +18,11 @@ sig = torch.empty((S, M), dtype=torch.int64, device="cuda")
 status = torch.zeros(2, dtype=torch.int64, device="cuda")
 L = _lib.load()
 main = torch.cuda.current_stream()
-for NC in (1, 2, 4):
+for NC, same in ((1, False), (2, False), (4, False), (2, True), (4, True), (8, True)):
     cut = [0] + [int(np.searchsorted(b.offsets, N * c // NC)) for c in range(1, NC)] + [S]
     streams = [torch.cuda.Stream() for _ in range(NC)]
+    if same:
+        streams = [streams[0]] * NC
     ts = []
     for rep in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -39,4 +41,5 @@ for NC in (1, 2, 4):
         e1.record(main)
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
-    print(v, "NC", NC, "ms", round(min(ts[1:]), 2), flush=True)
+    print(v, "NC", NC, "one stream" if same else "NC streams", "ms", round(min(ts[1:]), 2),
+          flush=True)
