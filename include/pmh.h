@@ -119,6 +119,23 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
                               const double* weights, const int64_t* offsets, int64_t nsets,
                               int64_t nelems, uint64_t* const* sig_outs,
                               int64_t* const* stats_outs, int64_t* err_set);
+
+/*
+ * Enqueue-only form of pmh_sketch_csr_host_multi: returns once the work is
+ * queued on internal streams, WITHOUT waiting for prior work on `stream`
+ * (the inputs are host buffers); `stream` is made to wait for its completion
+ * (copies back to the host buffers included).  Errors found while running
+ * land in d_status, which must be reset and settled before the first call
+ * (pmh_status_reset + a stream sync) and checked after the last.
+ * Host buffers must stay valid and unmodified until `stream` has passed this
+ * work, and should be pinned for the copies to overlap.  Consecutive calls
+ * use different internal streams, so one batch's H2D overlaps the previous
+ * batch's kernels (pipelined batches).
+ */
+int pmh_sketch_csr_host_multi_async(const int* algos, int nalgos, int64_t m, const uint64_t* ids,
+                                    const double* weights, const int64_t* offsets, int64_t nsets,
+                                    int64_t nelems, uint64_t* const* sig_outs,
+                                    int64_t* const* stats_outs, int64_t* d_status, void* stream);
 int pmh_sketch_csr_host(int algo, int64_t m, const uint64_t* ids,
                         const double* weights, const int64_t* offsets,
                         int64_t nsets, int64_t nelems, uint64_t* sig_out,

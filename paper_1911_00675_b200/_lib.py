@@ -36,6 +36,7 @@ UNWEIGHTED_IDS = {10, 11, 12, 13, 14, 15, 16, 17, 18}
 EXPORTS = ("pmh_version", "pmh_last_error", "pmh_sketch_csr", "pmh_sketch_csr_async",
            "pmh_sketch_csr_multi_async",
            "pmh_status_reset", "pmh_status_check", "pmh_sketch_csr_host", "pmh_sketch_csr_host_multi",
+           "pmh_sketch_csr_host_multi_async",
            "pmh_count_equal", "pmh_allpairs_tile", "pmh_allpairs_hist", "pmh_bbit",
            "pmh_bbit_words", "pmh_bbit_pack", "pmh_allpairs_bbit_hist",
            "pmh_mse_cell", "pmh_parse_weighted_text", "pmh_probe_alu_peak")
@@ -84,6 +85,9 @@ def load():
         L.pmh_sketch_csr_host_multi.argtypes = [_vp, ctypes.c_int, _i64, _vp, _vp, _vp, _i64,
                                                 _i64, _vp, _vp, _i64p]
         L.pmh_sketch_csr_host_multi.restype = ctypes.c_int
+        L.pmh_sketch_csr_host_multi_async.argtypes = [_vp, ctypes.c_int, _i64, _vp, _vp, _vp, _i64,
+                                                      _i64, _vp, _vp, _vp, _vp]
+        L.pmh_sketch_csr_host_multi_async.restype = ctypes.c_int
         L.pmh_count_equal.argtypes = [_vp, _vp, _i64, _i64, _vp, _vp]
         L.pmh_count_equal.restype = ctypes.c_int
         L.pmh_allpairs_tile.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _i64,

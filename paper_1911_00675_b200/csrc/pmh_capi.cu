@@ -543,10 +543,62 @@ int pmh_sketch_csr(int algo, int64_t m, const uint64_t* ids,
   return rc;
 }
 
-int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uint64_t* ids,
-                              const double* weights, const int64_t* offsets, int64_t nsets,
-                              int64_t nelems, uint64_t* const* sig_outs,
-                              int64_t* const* stats_outs, int64_t* err_set) {
+}  // extern "C"
+
+namespace {
+// per-device rotating pool of stream sets for the host entry points, so that
+// consecutive asynchronous calls (pipelined batches) never share a stream
+struct HostSet {
+  cudaStream_t st = nullptr, cin = nullptr, cout = nullptr, cst[8] = {};
+};
+constexpr int HOST_SETS = 3;
+std::map<int, std::vector<HostSet>> g_host_sets;
+std::map<int, unsigned> g_host_next;
+// per-device "kernels of the previous host call are done": a call's kernels
+// wait on it (compute stays in call order, no interference between batches)
+// while its copy-in does not (so it overlaps the previous batch's kernels)
+std::map<int, cudaEvent_t> g_compute_done;
+
+int get_compute_done(cudaEvent_t* out) {
+  int dev = 0;
+  PMH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaEvent_t& ev = g_compute_done[dev];
+  if (!ev) {
+    PMH_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    PMH_CUDA(cudaEventRecord(ev, 0));
+  }
+  *out = ev;
+  return PMH_OK;
+}
+
+int get_host_set(HostSet** out) {
+  int dev = 0;
+  PMH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  std::vector<HostSet>& v = g_host_sets[dev];
+  if (v.empty()) {
+    v.resize(HOST_SETS);
+    for (HostSet& h : v) {
+      PMH_CUDA(cudaStreamCreateWithFlags(&h.st, cudaStreamNonBlocking));
+      PMH_CUDA(cudaStreamCreateWithFlags(&h.cin, cudaStreamNonBlocking));
+      PMH_CUDA(cudaStreamCreateWithFlags(&h.cout, cudaStreamNonBlocking));
+      for (auto& c : h.cst) PMH_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+    }
+  }
+  *out = &v[g_host_next[dev]++ % HOST_SETS];
+  return PMH_OK;
+}
+}  // namespace
+
+extern "C" {
+
+// Host-buffer entry (synchronous when ext_status == nullptr, else enqueue-only
+// on `caller`, errors through ext_status).
+static int host_multi_impl(const int* algos, int nalgos, int64_t m, const uint64_t* ids,
+                           const double* weights, const int64_t* offsets, int64_t nsets,
+                           int64_t nelems, uint64_t* const* sig_outs, int64_t* const* stats_outs,
+                           int64_t* err_set, int64_t* ext_status, cudaStream_t caller) {
   if (err_set) *err_set = -1;
   if (nalgos < 1 || !algos || !sig_outs) return set_error(PMH_ERR_INVALID, "no algorithms");
   if (nsets < 0 || nelems < 0) return set_error(PMH_ERR_INVALID, "negative sizes");
@@ -565,10 +617,27 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
     }
   const bool weighted = any_weighted && weights;
   ensure_pool_retained();
-  cudaStream_t st = nullptr, cin = nullptr, cout = nullptr;
-  PMH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  PMH_CUDA(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
-  PMH_CUDA(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
+  HostSet* hs = nullptr;
+  {
+    int prc = get_host_set(&hs);
+    if (prc) return prc;
+  }
+  cudaStream_t st = hs->st, cin = hs->cin, cout = hs->cout;
+  cudaEvent_t compute_done = nullptr;
+  {
+    int erc = get_compute_done(&compute_done);
+    if (erc) return erc;
+  }
+  std::vector<cudaEvent_t> evs;
+  auto mkev = [&]() {
+    cudaEvent_t ev = nullptr;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    evs.push_back(ev);
+    return ev;
+  };
+  // asynchronous calls do not wait for prior work on the caller's stream
+  // (their inputs are host buffers): that is what lets batch i+1's copy-in
+  // run under batch i's kernels; only their completion is joined back
   const size_t bi = sizeof(uint64_t) * (size_t)nelems, bw = weighted ? sizeof(double) * (size_t)nelems : 0,
                bo = sizeof(int64_t) * (size_t)(nsets + 1), bs = sizeof(uint64_t) * (size_t)nsets * (size_t)m,
                bst = sizeof(int64_t) * 3 * (size_t)nsets;
@@ -577,22 +646,15 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
   char* d = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&d, bi + bw + bo + 16 + per_algo * (size_t)nalgos + 64, st);
   if (e != cudaSuccess) {
-    cudaStreamDestroy(st); cudaStreamDestroy(cin); cudaStreamDestroy(cout);
+    for (auto ev : evs) cudaEventDestroy(ev);
     return cuda_fail(e, "cudaMallocAsync");
   }
   uint64_t* d_ids = (uint64_t*)d;
   double* d_w = (double*)(d + bi);
   int64_t* d_off = (int64_t*)(d + bi + bw);
-  int64_t* d_status = (int64_t*)(d + bi + bw + bo);
+  int64_t* d_status = ext_status ? ext_status : (int64_t*)(d + bi + bw + bo);
   char* d_out = d + bi + bw + bo + 16;
   int rc = PMH_OK;
-  std::vector<cudaEvent_t> evs;
-  auto mkev = [&]() {
-    cudaEvent_t ev = nullptr;
-    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    evs.push_back(ev);
-    return ev;
-  };
   // Schedule (the copy-in is the long pole: 1.39 GB at ~55 GB/s for config 2):
   //  * offsets + status first, then the element arrays in NC set-chunks on
   //    the copy-in stream;
@@ -605,11 +667,14 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
   //    D2H overlapping whatever still runs.
   e = cudaMemcpyAsync(d_off, offsets, bo, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) rc = cuda_fail(e, "H2D offsets");
-  if (rc == PMH_OK) rc = pmh_status_reset(d_status, st);
+  if (rc == PMH_OK && !ext_status) rc = pmh_status_reset(d_status, st);
   cudaEvent_t ev_meta = mkev();
   cudaEventRecord(ev_meta, st);
   cudaStreamWaitEvent(cin, ev_meta, 0);
-  int NC = nsets >= 8 && nelems >= (1 << 20) ? 4 : 1;
+  // synchronous calls chunk the copy-in so the batch's own kernels start
+  // early; pipelined (async) calls copy in whole: their kernels wait for the
+  // previous batch's anyway, and whole-batch kernels are cheaper than chunked
+  int NC = (!ext_status && nsets >= 8 && nelems >= (1 << 20)) ? 4 : 1;
   if (const char* ev = getenv("PMH_H2D_CHUNKS")) {
     const int v = atoi(ev);
     if (v >= 1 && v <= 8 && nsets >= v) NC = v;
@@ -624,8 +689,7 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
   }
   auto chunkable = [&](int k) { return algos[k] != ALG_PMINHASH && algos[k] != ALG_MINHASH; };
   std::vector<cudaEvent_t> chunk_done;
-  cudaStream_t cst[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  for (int c = 0; c < NC; c++) cudaStreamCreateWithFlags(&cst[c], cudaStreamNonBlocking);
+  cudaStream_t* cst = hs->cst;
   for (int c = 0; c < NC && rc == PMH_OK; c++) {
     const int64_t e0 = offsets[cut[c]], e1 = offsets[cut[c + 1]];
     if (e1 > e0) {
@@ -640,6 +704,7 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
     cudaEvent_t ev = mkev();
     cudaEventRecord(ev, cin);
     cudaStreamWaitEvent(cst[c], ev, 0);
+    cudaStreamWaitEvent(cst[c], compute_done, 0);
     const int64_t ns = cut[c + 1] - cut[c];
     for (int k = 0; k < nalgos && rc == PMH_OK && ns > 0; k++) {
       if (!chunkable(k)) continue;
@@ -671,6 +736,7 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
   cudaEvent_t ev_in = mkev();
   cudaEventRecord(ev_in, cin);
   cudaStreamWaitEvent(st, ev_in, 0);
+  cudaStreamWaitEvent(st, compute_done, 0);
   for (int k = 0; k < nalgos && rc == PMH_OK; k++) {
     if (chunkable(k)) continue;
     char* outk = d_out + per_algo * (size_t)k;
@@ -689,17 +755,41 @@ int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uin
     }
   }
   for (cudaEvent_t evc : chunk_done) cudaStreamWaitEvent(st, evc, 0);
+  cudaEventRecord(compute_done, st);   // this call's kernels, for the next call
   cudaEvent_t ev_end = mkev();
   cudaEventRecord(ev_end, cout);
   cudaStreamWaitEvent(st, ev_end, 0);
+  if (ext_status) {
+    cudaFreeAsync(d, st);
+    cudaEvent_t join = mkev();
+    cudaEventRecord(join, st);
+    cudaStreamWaitEvent(caller, join, 0);
+    for (auto ev : evs) cudaEventDestroy(ev);   // released once complete
+    return rc;
+  }
   if (rc == PMH_OK) rc = pmh_status_check(d_status, err_set, st);
   cudaFreeAsync(d, st);
   e = cudaStreamSynchronize(st);
   for (auto ev : evs) cudaEventDestroy(ev);
-  for (int c = 0; c < NC; c++) if (cst[c]) cudaStreamDestroy(cst[c]);
-  cudaStreamDestroy(st); cudaStreamDestroy(cin); cudaStreamDestroy(cout);
   if (rc == PMH_OK && e != cudaSuccess) rc = cuda_fail(e, "sync");
   return rc;
+}
+
+int pmh_sketch_csr_host_multi(const int* algos, int nalgos, int64_t m, const uint64_t* ids,
+                              const double* weights, const int64_t* offsets, int64_t nsets,
+                              int64_t nelems, uint64_t* const* sig_outs,
+                              int64_t* const* stats_outs, int64_t* err_set) {
+  return host_multi_impl(algos, nalgos, m, ids, weights, offsets, nsets, nelems, sig_outs,
+                         stats_outs, err_set, nullptr, nullptr);
+}
+
+int pmh_sketch_csr_host_multi_async(const int* algos, int nalgos, int64_t m, const uint64_t* ids,
+                                    const double* weights, const int64_t* offsets, int64_t nsets,
+                                    int64_t nelems, uint64_t* const* sig_outs,
+                                    int64_t* const* stats_outs, int64_t* d_status, void* stream) {
+  if (!d_status) return set_error(PMH_ERR_INVALID, "status buffer required");
+  return host_multi_impl(algos, nalgos, m, ids, weights, offsets, nsets, nelems, sig_outs,
+                         stats_outs, nullptr, d_status, (cudaStream_t)stream);
 }
 
 int pmh_sketch_csr_host(int algo, int64_t m, const uint64_t* ids,

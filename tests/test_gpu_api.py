@@ -345,3 +345,41 @@ def test_text_ingestion_to_signatures(tmp_path):
                               to_device_i64(b.offsets), 128)
         ref, _ = orc.sketch_csr(algo, 128, b.ids, b.weights, b.offsets)
         assert np.array_equal(sig.cpu().numpy().view(np.uint64), ref)
+
+
+def test_host_multi_async_pipelined_batches():
+    """Several pmh_sketch_csr_host_multi_async batches in flight (pinned host
+    buffers, one stream) == the synchronous call, batch by batch."""
+    import ctypes
+    import torch
+    from paper_1911_00675_b200 import _lib
+    from paper_1911_00675_b200.batch import sketch_csr_multi
+    L = _lib.load()
+    algos = ["probminhash3", "pminhash", "probminhash2"]
+    aids = (ctypes.c_int * len(algos))(*[_lib.ALG[a] for a in algos])
+    batches = [datagen.random_sets(70 + k, list(np.exp(np.linspace(0, 8.5, 30)).astype(int) + 1),
+                                   "uniform") for k in range(3)]
+    keep, outs = [], []
+    status = torch.zeros(2, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(s.cuda_stream)
+    _lib.check(L.pmh_status_reset(status.data_ptr(), sp))
+    s.synchronize()
+    for b in batches:
+        h_ids = torch.from_numpy(b.ids.view(np.int64)).pin_memory()
+        h_w = torch.from_numpy(b.weights).pin_memory()
+        h_off = torch.from_numpy(b.offsets).pin_memory()
+        o = [torch.empty((b.nsets, 128), dtype=torch.int64).pin_memory() for _ in algos]
+        ptrs = (ctypes.c_void_p * len(algos))(*[t.data_ptr() for t in o])
+        _lib.check(L.pmh_sketch_csr_host_multi_async(aids, len(algos), 128, h_ids.data_ptr(),
+                                                     h_w.data_ptr(), h_off.data_ptr(), b.nsets,
+                                                     b.nelems, ptrs, None, status.data_ptr(), sp))
+        keep.append((h_ids, h_w, h_off, ptrs))
+        outs.append(o)
+    s.synchronize()
+    err = ctypes.c_int64(-1)
+    _lib.check(L.pmh_status_check(status.data_ptr(), ctypes.byref(err), sp), err.value)
+    for b, o in zip(batches, outs):
+        ref, _ = sketch_csr_multi(algos, 128, b.ids, b.weights, b.offsets)
+        for got, r in zip(o, ref):
+            assert np.array_equal(got.numpy().view(np.uint64), r)
