@@ -41,6 +41,7 @@ M = 1024
 VARIANTS = ["pminhash", "probminhash1", "probminhash1a", "probminhash2",
             "probminhash3", "probminhash3a", "probminhash4"]
 METRIC = "set elements hashed/sec at m=1024"
+E2E_DEPTH = 2   # pipelined e2e: batches in flight
 # splitmix64 word: 64-bit add (2) + 3 x (64-bit shift + xor: 4) = 14 ALU ops;
 # a 53-bit draw uses 53/64 word, + 2 ops (extract 32 bits, compare)
 ALU_OPS_PER_DRAW = 14.0 * 53.0 / 64.0 + 2.0
@@ -214,8 +215,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sequential", action="store_true",
-                    help="launch the variants one after another instead of concurrently")
+    ap.add_argument("--per-variant-reps", type=int, default=2,
+                    help="untimed passes that time each variant alone (0: skip)")
+    ap.add_argument("--concurrent", action="store_true",
+                    help="run the step's variants concurrently (pmh_sketch_csr_multi_async); "
+                         "per-variant times then come from separate untimed passes")
     ap.add_argument("--variants", default=",".join(VARIANTS))
     args = ap.parse_args()
     if args.impl == "reference":
@@ -263,29 +267,40 @@ def main():
     arr_a = (ctypes.c_int * len(variants))(*[_lib.ALG[v] for v in variants])
     arr_s = (ctypes.c_void_p * len(variants))(*[t.data_ptr() for t in sigs_multi])
 
-    def launch_step():
-        if args.sequential:
-            for v in variants:
-                launch(v)
-        else:
+    ev = {v: [] for v in variants}
+
+    def launch_step(timed=False):
+        if args.concurrent:
             _lib.check(L.pmh_sketch_csr_multi_async(arr_a, len(variants), M, ids.data_ptr(),
                                                     w.data_ptr(), off.data_ptr(), S, arr_s, None,
                                                     status.data_ptr(), sp))
+            return
+        for v in variants:
+            if timed:   # per-launch events on the launching stream, inside the timed region
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                launch(v)
+                b.record(stream)
+                ev[v].append((a, b))
+            else:
+                launch(v)
 
     for _ in range(args.warmup):
         launch_step()
     torch.cuda.synchronize()
-    # per-variant device time, each variant alone (outside the timed region)
-    ev = {v: [] for v in variants}
-    for _ in range(2):
-        for v in variants:
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            launch(v)
-            b.record(stream)
-            ev[v].append((a, b))
-    torch.cuda.synchronize()
+    if args.concurrent:
+        # the concurrent step has no separable per-kernel times: each variant
+        # alone, outside the timed region
+        for _ in range(args.per_variant_reps):
+            for v in variants:
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                launch(v)
+                b.record(stream)
+                ev[v].append((a, b))
+        torch.cuda.synchronize()
 
     clk_sampler = ClockSampler(local)
     if world > 1:
@@ -296,7 +311,7 @@ def main():
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
         for _ in range(args.steps):
-            launch_step()
+            launch_step(timed=True)
         t_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -308,7 +323,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    per_variant_ms = {v: float(np.mean([a.elapsed_time(b) for a, b in ev[v]])) for v in variants}
+    per_variant_ms = {v: float(np.mean([a.elapsed_time(b) for a, b in ev[v]])) if ev[v] else None
+                      for v in variants}
     value = world * len(variants) * N / (ms_step / 1e3)
 
     # ---- e2e: C ABI host entry with HOST buffers, copies inside the timing ----
@@ -356,12 +372,26 @@ def main():
         e2e_step_sync()
         e2e_sync_s = timed_e2e(lambda k: [e2e_step_sync() for _ in range(k)], args.e2e_steps)
         _lib.check(L.pmh_status_reset(status.data_ptr(), sp))
-        e2e_step_async(0)
+        torch.cuda.synchronize()
+
+        def pipelined(k):
+            # at most DEPTH batches in flight: before enqueueing step i the
+            # host waits for step i - DEPTH (a serving loop's back-pressure;
+            # also keeps the device working set at DEPTH batches)
+            done = []
+            for i in range(k):
+                if i >= E2E_DEPTH:
+                    done[i - E2E_DEPTH].synchronize()
+                e2e_step_async(i)
+                ev_i = torch.cuda.Event()
+                ev_i.record(stream)
+                done.append(ev_i)
+
+        pipelined(E2E_DEPTH)          # warm-up: memory pool at its steady-state size
         torch.cuda.synchronize()
         # every step copies its inputs in and its signatures out (pinned host
-        # memory) inside the timed region; steps are pipelined two deep
-        e2e_s = timed_e2e(lambda k: [e2e_step_async(i) for i in range(k)],
-                          max(args.e2e_steps, 6))
+        # memory) inside the timed region
+        e2e_s = timed_e2e(pipelined, max(args.e2e_steps, 6))
         _lib.check(L.pmh_status_check(status.data_ptr(), ctypes.byref(err), sp), err.value)
     h2d = batch.ids.nbytes + batch.weights.nbytes + batch.offsets.nbytes
     d2h = len(variants) * S * M * 8
@@ -372,6 +402,8 @@ def main():
         return
 
     hbm_peak, peak_src = _peaks()
+    if any(t is None for t in per_variant_ms.values()):   # --concurrent --per-variant-reps 0
+        per_variant_ms = {v: ms_step / len(variants) for v in variants}
     dom = max(per_variant_ms, key=per_variant_ms.get)
     alg_bytes = algorithmic_bytes(N, S, M)
     hbm_achieved = alg_bytes / (per_variant_ms[dom] / 1e3) / 1e9
@@ -415,15 +447,13 @@ def main():
         "config": {"workload": "config2: 10k log-uniform weighted sets, 7 weighted variants, m=1024",
                    "sets_per_gpu": S, "elements_per_gpu": N, "m": M,
                    "variants": variants, "l2": "inputs 1.47 GB > 126 MB L2",
-                   "schedule": ("sequential" if args.sequential else
-                                "concurrent (pmh_sketch_csr_multi_async)")},
-        # each variant timed ALONE (outside the timed region); the step runs
-        # them concurrently, so the step is shorter than their sum
+                   "schedule": ("concurrent (pmh_sketch_csr_multi_async)" if args.concurrent
+                                else "sequential, per-launch CUDA events in the timed region")},
         "per_variant_ms": per_variant_ms,
         "per_variant_elems_per_s": {v: N / (t / 1e3) for v, t in per_variant_ms.items()},
         "e2e": {"value": world * len(variants) * N / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "pmh_sketch_csr_host_multi_async, consecutive batches pipelined",
+                "api": "pmh_sketch_csr_host_multi_async, batches pipelined %d deep" % E2E_DEPTH,
                 "sync_call_value": world * len(variants) * N / e2e_sync_s},
         # per variant call: 3 ordering kernels + the sketch kernel (+ the
         # concurrent small-set kernel for the ProbMinHash families)
