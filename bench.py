@@ -325,7 +325,13 @@ def main():
     ms_step = ms_total / args.steps
     per_variant_ms = {v: float(np.mean([a.elapsed_time(b) for a, b in ev[v]])) if ev[v] else None
                       for v in variants}
-    value = world * len(variants) * N / (ms_step / 1e3)
+    # whole-job elements: every rank sketches its own batch (seed 2 + rank)
+    n_total = N
+    if world > 1:
+        t = torch.tensor([float(N)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        n_total = float(t.item())
+    value = len(variants) * n_total / (ms_step / 1e3)
 
     # ---- e2e: C ABI host entry with HOST buffers, copies inside the timing ----
     # one step = the host batch sketched by all variants through
@@ -451,10 +457,10 @@ def main():
                                 else "sequential, per-launch CUDA events in the timed region")},
         "per_variant_ms": per_variant_ms,
         "per_variant_elems_per_s": {v: N / (t / 1e3) for v, t in per_variant_ms.items()},
-        "e2e": {"value": world * len(variants) * N / e2e_s, "unit": UNIT,
+        "e2e": {"value": len(variants) * n_total / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "pmh_sketch_csr_host_multi_async, batches pipelined %d deep" % E2E_DEPTH,
-                "sync_call_value": world * len(variants) * N / e2e_sync_s},
+                "sync_call_value": len(variants) * n_total / e2e_sync_s},
         # per variant call: 3 ordering kernels + the sketch kernel (+ the
         # concurrent small-set kernel for the ProbMinHash families)
         "gpu_launches": args.steps * sum(4 if v == "pminhash" else 5 for v in variants),
