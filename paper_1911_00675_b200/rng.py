@@ -140,8 +140,54 @@ class RandomStream:
                 raise RandomnessFailureError(
                     "truncated exponential rejection loop exceeded its cap")
 
+    def _words_np(self, count: int) -> np.ndarray:
+        """The next `count` stream words (vectorised next_u64)."""
+        k = np.arange(1, count + 1, dtype=np.uint64)
+        with np.errstate(over="ignore"):
+            x = np.uint64(self._s) + k * np.uint64(_GOLDEN)
+            z = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            z = z ^ (z >> np.uint64(31))
+        self._s = (self._s + count * _GOLDEN) & _MASK
+        self._words += count
+        return z
+
+    def _bits53_np(self, count: int) -> np.ndarray:
+        """`count` consecutive 53-bit draws of _next_bits(53), vectorised:
+        draw i is bits [53 i, 53 i + 53) of (buffered bits, then whole words,
+        LSB first)."""
+        out = np.empty(count, np.uint64)
+        if count == 0:
+            return out
+        i0 = 0
+        if self._nb >= 53:           # the first draw fits the buffer
+            out[0] = self._next_bits(53)
+            i0 = 1
+        if i0 == count:
+            return out
+        nb, buf = self._nb, self._buf
+        need = 53 * (count - i0) - nb                 # bits to take from new words
+        nw = -(-need // 64)
+        w = np.concatenate([self._words_np(nw), np.zeros(1, np.uint64)])
+        q = np.arange(count - i0, dtype=np.int64) * 53 - nb   # offset into the words
+        first = q < 0                                  # straddles buffer and words
+        qq = np.where(first, 0, q)
+        wi, sh = qq >> 6, (qq & 63).astype(np.uint64)
+        lo = w[wi] >> sh
+        hi = np.where(sh > 0, w[wi + 1] << ((np.uint64(64) - sh) & np.uint64(63)), np.uint64(0))
+        v = (lo | hi) & np.uint64((1 << 53) - 1)
+        if first[0]:                                   # buffer bits + low bits of word 0
+            v[0] = np.uint64((buf | ((int(w[0]) << nb) & _MASK)) & ((1 << 53) - 1))
+        out[i0:] = v
+        used = 53 * (count - i0) - nb                  # bits consumed from the new words
+        rem = 64 * nw - used
+        last = int(w[nw - 1])
+        self._buf = last >> (64 - rem) if rem else 0
+        self._nb = rem
+        return out
+
     def uniform01_batch(self, count: int) -> np.ndarray:
-        return np.array([self.next_uniform01() for _ in range(count)], np.float64)
+        return self._bits53_np(count).astype(np.float64) * 1.1102230246251565e-16
 
     def uniform_int_batch(self, n: int, count: int) -> np.ndarray:
         return np.array([self.next_uniform_int(n) for _ in range(count)], np.int64)
@@ -157,7 +203,8 @@ class RandomStream:
                         np.float64)
 
     def u64_batch(self, count: int) -> np.ndarray:
-        return np.array([self.next_u64() for _ in range(count)], np.uint64)
+        # whole words; the bit buffer is left as it is (K:242-245)
+        return self._words_np(count)
 
     @property
     def words_generated(self) -> int:

@@ -104,3 +104,15 @@ def test_gpu_criterion_03_superminhash_variance_law():
             exp = improvement_factor(m, 3) * r.jp * (1 - r.jp) / m
             worst = max(worst, abs((r.mse - exp) / H.mse_sampling_sd(r.jp, m, r.pairs)))
     assert worst <= Z_BAND
+
+
+def test_gpu_timing_experiment_rows():
+    cfg = H.ExperimentConfig(algorithms=("probminhash3", "pminhash"), m_values=(64,),
+                             n_values=(10, 1000), reps=50,
+                             distribution=H.WeightDistributionSpec("pareto", 2.0))
+    rows = H.run_timing_experiment(cfg)
+    assert [(r.algorithm, r.m, r.n) for r in rows] == [
+        ("probminhash3", 64, 10), ("probminhash3", 64, 1000), ("pminhash", 64, 10),
+        ("pminhash", 64, 1000)]
+    assert all(r.mean_ns > 0 for r in rows)
+    assert H.timing_csv(rows).count("\n") == 5

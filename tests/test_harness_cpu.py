@@ -108,3 +108,26 @@ def test_mse_cell_fails_loudly_without_cuda():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         H.run_mse_cell("probminhash1", 16, "skew2", 4, 0)
+
+
+def test_timing_inputs_match_reference_stream():
+    """The timing grid's inputs come from the same seeded stream as the
+    reference's (harness.py:293-321): ids = whole words, weights = Pareto
+    inverse CDF over the following 53-bit draws."""
+    from paper_1911_00675_b200.rng import RandomStream
+    dist = H.WeightDistributionSpec("pareto", 1.5)
+    st = RandomStream(H.cell_seed(0, "timing", "probminhash4", 64, 7))
+    ids, w = H._random_input(7, dist, st)
+    ref = RandomStream(H.cell_seed(0, "timing", "probminhash4", 64, 7))
+    exp_ids = np.array([ref.next_u64() for _ in range(7)], np.uint64)
+    exp_w = np.array([(1.0 - ref.next_uniform01()) ** (-1.0 / 1.5) for _ in range(7)])
+    assert np.array_equal(ids, exp_ids) and np.array_equal(w, exp_w)
+    assert dist.name == "pareto(1,1.5)" and H.WeightDistributionSpec().name == "unweighted"
+    with pytest.raises(InvalidParamsError):
+        H.WeightDistributionSpec("zipf")
+    with pytest.raises(InvalidParamsError):
+        H.run_timing_experiment(H.ExperimentConfig())          # no n_values
+    with pytest.raises(InvalidParamsError):
+        H.run_buffer_experiment(H.ExperimentConfig(n_values=(10,)))
+    assert H.timing_csv([H.TimingRow("pminhash", 16, 10, 12.5)]) == \
+        "algorithm,m,n,mean_ns\npminhash,16,10,12.5\n"
