@@ -46,6 +46,12 @@ int cuda_fail(cudaError_t e, const char* where) {
     cudaError_t _e = (call);                            \
     if (_e != cudaSuccess) return cuda_fail(_e, #call); \
   } while (0)
+// for functions returning cudaError_t
+#define PMH_CUDA_E(call)                 \
+  do {                                   \
+    cudaError_t _e = (call);             \
+    if (_e != cudaSuccess) return _e;    \
+  } while (0)
 
 
 // ---- constant tables (glibc on the host, uploaded once per device and m) --
@@ -264,6 +270,48 @@ int get_aux(AuxStream** out, int slot = 0) {
   return PMH_OK;
 }
 
+// P-MinHash with its largest sets split across CTAs: prep (part counts) and
+// table init on `st`, then the split kernel on `st` beside the regular kernel
+// (remaining sets) on the auxiliary stream, then the ids of the split sets.
+template <bool EXPO>
+cudaError_t launch_pminhash_split(PMinArgs a, const unsigned* big_count, int64_t split_n,
+                                  int64_t split_cap, cudaStream_t st, int aux_slot) {
+  AuxStream* aux = nullptr;
+  if (get_aux(&aux, aux_slot) != PMH_OK) return cudaErrorUnknown;
+  char* ws = nullptr;
+  const size_t bt = sizeof(Slot) * (size_t)split_cap * (size_t)a.m;
+  const size_t bp = sizeof(int64_t) * (size_t)(split_cap + 1);
+  cudaError_t e = cudaMallocAsync((void**)&ws, bt + bp + 4 * sizeof(long long), st);
+  if (e != cudaSuccess) return e;
+  a.big_count = big_count;
+  a.split_cap = split_cap;
+  a.split_n = split_n;
+  a.gtab = reinterpret_cast<Slot*>(ws);
+  a.part_base = reinterpret_cast<int64_t*>(ws + bt);
+  a.split_info = reinterpret_cast<long long*>(ws + bt + bp);
+  const size_t smem = sizeof(Slot) * (size_t)a.m + sizeof(uint2) * PM64_CQ * (PMIN_THREADS / 32);
+  if ((e = cudaFuncSetAttribute(pminhash64_split_kernel<EXPO>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+    return e;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pminhash64_split_kernel<EXPO>,
+                                                PMIN_THREADS, smem);
+  if (per_sm < 1) per_sm = 1;
+  pm64_split_prep_kernel<<<1, 1024, 0, st>>>(a, (long long)sms * per_sm);
+  pm64_split_init_kernel<<<(unsigned)(sms * 4), 256, 0, st>>>(a);
+  PMH_CUDA_E(cudaEventRecord(aux->fork, st));
+  PMH_CUDA_E(cudaStreamWaitEvent(aux->s, aux->fork, 0));
+  if ((e = launch_pminhash<EXPO>(a, aux->s)) != cudaSuccess) return e;   // remaining sets
+  pminhash64_split_kernel<EXPO><<<(unsigned)(sms * per_sm), PMIN_THREADS, smem, st>>>(a);
+  pm64_split_finalize_kernel<<<(unsigned)(sms * 4), 256, 0, st>>>(a);
+  PMH_CUDA_E(cudaEventRecord(aux->join, aux->s));
+  PMH_CUDA_E(cudaStreamWaitEvent(st, aux->join, 0));
+  cudaFreeAsync(ws, st);
+  return cudaGetLastError();
+}
+
 // per-device pool of internal streams for the concurrent multi-variant entry
 struct LanePool {
   std::vector<cudaStream_t> s;
@@ -444,17 +492,34 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
     return PMH_OK;
   }
   const bool pmin = algo == ALG_PMINHASH || algo == ALG_MINHASH;
+  // P-MinHash splits its largest sets across CTAs (static kernel only): sets
+  // with n >= split_n (a power of two, so with cost offset 0 they form a
+  // prefix of the LPT order), at most split_cap of them
+  const bool pm_static = pmin && m % PM64_C == 0 && m / PM64_C <= PMIN_THREADS;
+  int64_t split_n = 16384, split_cap = 1024;
+  if (const char* ev = getenv("PMH_PM64_SPLIT_N")) split_n = atoll(ev);
+  if (const char* ev = getenv("PMH_PM64_SPLIT_CAP")) split_cap = atoll(ev);
+  if (split_cap > (1LL << 24) / m) split_cap = (1LL << 24) / m;
+  const bool pm_split = pm_static && split_n >= 64 && (split_n & (split_n - 1)) == 0 &&
+                        split_cap > 0;
   OrderWs ow;
   // cost offset: ProbMinHash families pay ~m ln m points per set regardless of n
   e = build_order(offsets, nsets, pmin ? 0 : (int64_t)(7.0 * (double)m), pmin ? -1 : small_n_for(m),
-                  4096, st, &ow);
+                  pm_split ? split_n : 4096, st, &ow);
   if (e != cudaSuccess) return cuda_fail(e, "set ordering");
   int32_t* order = ow.order;
   void* order_ws = ow.mem;
   if (pmin) {
     PMinArgs a{ids, algo == ALG_PMINHASH ? weights : nullptr, offsets, order, nsets, m,
                sig_out, stats_out, d_err_set, 4u};
-    e = algo == ALG_PMINHASH ? launch_pminhash<true>(a, st) : launch_pminhash<false>(a, st);
+    if (!pm_split) {
+      e = algo == ALG_PMINHASH ? launch_pminhash<true>(a, st) : launch_pminhash<false>(a, st);
+    } else {
+      e = algo == ALG_PMINHASH ? launch_pminhash_split<true>(a, ow.counts + 1, split_n, split_cap,
+                                                             st, aux_slot)
+                               : launch_pminhash_split<false>(a, ow.counts + 1, split_n,
+                                                              split_cap, st, aux_slot);
+    }
   } else {
     const Tables* tp = nullptr;
     int rc = get_tables(fam, m, &tp);

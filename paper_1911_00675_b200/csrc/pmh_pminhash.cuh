@@ -29,6 +29,14 @@ struct PMinArgs {
   int64_t* stats;
   long long* err_set;
   uint32_t k4;              // == 4, opaque to the compiler (see mix64_bal)
+  // split large sets (static kernel only; all null/0 when not splitting):
+  // order[0, *nsplit) are the split sets, each in parts of <= split_n elements
+  const unsigned* big_count;   // device: sets with n >= split_n (an order prefix)
+  int64_t split_cap;           // at most this many sets are split (gtab rows)
+  int64_t split_n;
+  Slot* gtab;                  // [split_cap, m] merged minima of the split sets
+  int64_t* part_base;          // [split_cap + 1] prefix of parts per split set
+  long long* split_info;       // [0] = nsplit, [1] = total parts, [2] = work counter
 };
 
 constexpr int PMIN_THREADS = 256;
@@ -275,6 +283,158 @@ __device__ __forceinline__ uint64_t add_fma_t(uint64_t st, uint32_t one) {
 #define add_fma(st, one, clo, chi) add_fma_t<clo, chi>(st, one)
 
 
+// Exact (verified) minima of elements [e0, e1) of the set at `off` into the
+// shared `table` (all threads of the CTA; returns after a final barrier).
+// The threshold guess uses the range's own weight sum: the minima over a
+// range are Exp(W_range), and the verification makes any guess exact-safe.
+template <bool EXPO>
+__device__ __forceinline__ void pm64_range(const PMinArgs& a, int64_t off, int64_t e0, int64_t e1,
+                                           Slot* table, unsigned char* smem, uint32_t* s_onep,
+                                           double* s_wsum, int* s_retryp) {
+  const int64_t m = a.m;
+  const int tpg = (int)(m / PM64_C);               // threads per group
+  const int groups = PMIN_THREADS / tpg;
+  const int g = threadIdx.x / tpg, t = threadIdx.x % tpg;
+  const bool active = g < groups;
+  const double two53m = 9007199254740992.0 * 1.0000000000009095;  // 2^53 (1 + 2^-40)
+  const uint64_t wbase = 53ULL * (uint64_t)t + 1ULL;                // first word (1-based)
+  uint32_t& s_one = *s_onep;
+  int& s_retry = *s_retryp;
+  // Threshold guess: every slot minimum is Exp(W) (W = total weight), so
+  // tg = (ln m + PM64_TCONST) / W bounds all m of them unless a rare set
+  // (~m e^-(ln m + c) = e^-c) exceeds it; the final table is verified and
+  // such a set re-runs with 4 tg, then without a bound.  Draws above tg are
+  // never candidates, so no element starts with an infinite threshold.
+  double W;
+  if (EXPO && a.w) {
+    double p = 0.0;
+    for (int64_t k = e0 + threadIdx.x; k < e1; k += blockDim.x) p += __ldg(&a.w[off + k]);
+    for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+    if ((threadIdx.x & 31) == 0) s_wsum[threadIdx.x >> 5] = p;
+    __syncthreads();
+    W = 0.0;
+    for (int k = 0; k < PMIN_THREADS / 32; k++) W += s_wsum[k];
+  } else {
+    W = (double)(e1 - e0);
+  }
+  const double inf_d = __longlong_as_double(0x7FF0000000000000LL);
+  double tg = (log((double)m) + PM64_TCONST) / W;
+  if (!(tg > 0.0) || !(tg < 1e300)) tg = inf_d;
+  for (int attempt = 0;; attempt++) {
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+      table[k].h = EMPTY_H;
+      table[k].idx = EMPTY_IDX;
+    }
+    __syncthreads();
+    if (active) {
+      const uint64_t* ids = a.ids + off;
+      const double* ws = (EXPO && a.w) ? a.w + off : nullptr;
+      double tmax = tg;
+      int since = 0;
+      // groups per warp (2 when m = 1024): the trip count is made warp-uniform
+      // so a full-warp __syncwarp can reconverge the lanes every element
+      const int gpw = tpg >= 32 ? 1 : 32 / tpg;
+      const int gsub = g % gpw;
+      int64_t ew = e0 + g - gsub;                  // first group of this warp
+      int64_t e = ew + gsub;
+      // per-warp candidate queue (warp-aligned groups only: the trip count
+      // and every lane must be warp-uniform for the collectives)
+      const bool use_q = PM64_USEQ && ((32 % tpg == 0) || (tpg % 32 == 0));
+      const int lane = threadIdx.x & 31;
+      uint2* cq = reinterpret_cast<uint2*>(smem + sizeof(Slot) * m) + (threadIdx.x >> 5) * PM64_CQ;
+      int qn = 0;
+      uint64_t id_n = e < e1 ? __ldg(&ids[e]) : 0;
+      double w_n = (ws && e < e1) ? __ldg(&ws[e]) : 1.0;
+      for (; ew < e1; ew += groups) {
+        e = ew + gsub;
+        const bool live = e < e1;
+        const uint64_t id = id_n;
+        const double w = w_n;
+        if (e + groups < e1) {                     // prefetch the next element
+          id_n = __ldg(&ids[e + groups]);
+          if (ws) w_n = __ldg(&ws[e + groups]);
+        }
+        const double tb = tmax * (w * two53m);
+        // b < Tb = floor(tb) + 1  =>  b >> 21 <= tb >> 21
+        const uint32_t tbh = tb < 9007199254740992.0 ? (uint32_t)((uint64_t)tb >> 21)
+                                                      : 0xFFFFFFFFu;
+        uint64_t st = id + wbase * GOLDEN;
+        const uint32_t one = *(volatile uint32_t*)&s_one;
+        uint32_t c_lo = 0, c_hi = 0;
+        const uint32_t k4 = a.k4;
+#define MIX mix64
+#include "pm64_body.inc"
+#undef MIX
+        const uint64_t cand = live ? (((uint64_t)c_hi << 32) | c_lo) : 0ULL;
+        // candidates are cheap (1-2 stream words + a compare against the
+        // slot's own minimum) but scattered: a few lanes per warp-step.  They
+        // are queued per warp and checked 32 at a time with every lane busy;
+        // only the all-candidate start (infinite threshold) or a queue
+        // overflow runs them in place.  The threshold refresh is periodic --
+        // a stale, larger tmax only admits more candidates.
+        const bool inf = !(tmax < 1e300);
+        if (use_q) {
+          const int c = __popcll(cand);
+          int x = c;                                   // inclusive lane scan
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          const int total = __shfl_sync(0xffffffffu, x, 31);
+          const bool direct = __any_sync(0xffffffffu, inf) || qn + total > PM64_CQ;
+          if (direct) {
+            if (cand) pm64_candidates<EXPO>(cand, id, w, (uint32_t)e, t, tpg, table);
+          } else if (total) {
+            int pos = qn + x - c;
+            for (uint64_t cb = cand; cb; cb &= cb - 1)
+              cq[pos++] = make_uint2((uint32_t)e, ((uint32_t)t << 6) | (uint32_t)(__ffsll((long long)cb) - 1));
+            qn += total;
+            __syncwarp();
+            while (qn >= 32) {
+              qn -= 32;
+              const uint2 en = cq[qn + lane];
+              __syncwarp();
+              pm64_check_entry<EXPO>(en, ids, ws, tpg, table);
+            }
+          }
+        } else if (cand) {
+          pm64_candidates<EXPO>(cand, id, w, (uint32_t)e, t, tpg, table);
+        }
+        if (++since >= PM64_REFRESH || (cand && inf)) {
+          tmax = fmin(pm64_tmax(table, t, tpg), tg);
+          since = 0;
+        }
+        // reconverge: lanes that took the candidate path would otherwise run
+        // the straight-line body out of phase (independent thread scheduling)
+        __syncwarp();
+      }
+      if (use_q && lane < qn) pm64_check_entry<EXPO>(cq[lane], ids, ws, tpg, table);
+    }
+    __syncthreads();
+    // verification: every slot filled and <= tg
+    {
+      unsigned long long mx = 0;
+      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+        const unsigned long long h = table[k].h;
+        mx = h > mx ? h : mx;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = v > mx ? v : mx;
+      }
+      if (threadIdx.x == 0) s_retry = 0;
+      __syncthreads();
+      if ((threadIdx.x & 31) == 0 && __longlong_as_double((long long)mx) > tg) atomicOr(&s_retry, 1);
+      __syncthreads();
+      const int retry = s_retry;
+      __syncthreads();
+      if (!retry || !(tg < 1e300)) break;
+      tg = attempt >= 1 ? inf_d : tg * 4.0;
+    }
+  }
+}
+
 #ifndef PM64_MINBLOCKS
 #define PM64_MINBLOCKS 4   // 64 registers, 4 CTAs (32 warps) per SM
 #endif
@@ -282,20 +442,16 @@ template <bool EXPO>
 __global__ void __launch_bounds__(PMIN_THREADS, PM64_MINBLOCKS) pminhash64_kernel(PMinArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int64_t m = a.m;
-  const int tpg = (int)(m / PM64_C);               // threads per group
-  const int groups = PMIN_THREADS / tpg;
-  const int g = threadIdx.x / tpg, t = threadIdx.x % tpg;
-  const bool active = g < groups;
+  const int tpg = (int)(m / PM64_C);
   Slot* table = reinterpret_cast<Slot*>(smem);
-  const double two53m = 9007199254740992.0 * 1.0000000000009095;  // 2^53 (1 + 2^-40)
-  const uint64_t wbase = 53ULL * (uint64_t)t + 1ULL;                // first word (1-based)
   __shared__ uint32_t s_one;
   __shared__ double s_wsum[PMIN_THREADS / 32];
   __shared__ int s_retry;
   if (threadIdx.x == 0) s_one = 1u;
   __syncthreads();
-
-  for (int64_t bs = blockIdx.x; bs < a.nsets; bs += gridDim.x) {
+  // the split sets (an order prefix) belong to pminhash64_split_kernel
+  const int64_t first = a.split_info ? (int64_t)a.split_info[0] : 0;
+  for (int64_t bs = first + blockIdx.x; bs < a.nsets; bs += gridDim.x) {
     const int64_t s = a.order ? (int64_t)a.order[bs] : bs;
     const int64_t off = a.offsets[s];
     const int64_t n = a.offsets[s + 1] - off;
@@ -303,139 +459,7 @@ __global__ void __launch_bounds__(PMIN_THREADS, PM64_MINBLOCKS) pminhash64_kerne
       if (threadIdx.x == 0) atomicMin(a.err_set, (long long)s);
       continue;
     }
-    // Threshold guess: every slot minimum is Exp(W) (W = total weight), so
-    // tg = (ln m + PM64_TCONST) / W bounds all m of them unless a rare set
-    // (~m e^-(ln m + c) = e^-c) exceeds it; the final table is verified and
-    // such a set re-runs with 4 tg, then without a bound.  Draws above tg are
-    // never candidates, so no element starts with an infinite threshold.
-    double W;
-    if (EXPO && a.w) {
-      double p = 0.0;
-      for (int64_t k = threadIdx.x; k < n; k += blockDim.x) p += __ldg(&a.w[off + k]);
-      for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-      if ((threadIdx.x & 31) == 0) s_wsum[threadIdx.x >> 5] = p;
-      __syncthreads();
-      W = 0.0;
-      for (int k = 0; k < PMIN_THREADS / 32; k++) W += s_wsum[k];
-    } else {
-      W = (double)n;
-    }
-    const double inf_d = __longlong_as_double(0x7FF0000000000000LL);
-    double tg = (log((double)m) + PM64_TCONST) / W;
-    if (!(tg > 0.0) || !(tg < 1e300)) tg = inf_d;
-    for (int attempt = 0;; attempt++) {
-      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-        table[k].h = EMPTY_H;
-        table[k].idx = EMPTY_IDX;
-      }
-      __syncthreads();
-      if (active) {
-        const uint64_t* ids = a.ids + off;
-        const double* ws = (EXPO && a.w) ? a.w + off : nullptr;
-        double tmax = tg;
-        int since = 0;
-        // groups per warp (2 when m = 1024): the trip count is made warp-uniform
-        // so a full-warp __syncwarp can reconverge the lanes every element
-        const int gpw = tpg >= 32 ? 1 : 32 / tpg;
-        const int gsub = g % gpw;
-        int64_t ew = g - gsub;                       // first group of this warp
-        int64_t e = ew + gsub;
-        // per-warp candidate queue (warp-aligned groups only: the trip count
-        // and every lane must be warp-uniform for the collectives)
-        const bool use_q = PM64_USEQ && ((32 % tpg == 0) || (tpg % 32 == 0));
-        const int lane = threadIdx.x & 31;
-        uint2* cq = reinterpret_cast<uint2*>(smem + sizeof(Slot) * m) + (threadIdx.x >> 5) * PM64_CQ;
-        int qn = 0;
-        uint64_t id_n = e < n ? __ldg(&ids[e]) : 0;
-        double w_n = (ws && e < n) ? __ldg(&ws[e]) : 1.0;
-        for (; ew < n; ew += groups) {
-          e = ew + gsub;
-          const bool live = e < n;
-          const uint64_t id = id_n;
-          const double w = w_n;
-          if (e + groups < n) {                      // prefetch the next element
-            id_n = __ldg(&ids[e + groups]);
-            if (ws) w_n = __ldg(&ws[e + groups]);
-          }
-          const double tb = tmax * (w * two53m);
-          // b < Tb = floor(tb) + 1  =>  b >> 21 <= tb >> 21
-          const uint32_t tbh = tb < 9007199254740992.0 ? (uint32_t)((uint64_t)tb >> 21)
-                                                        : 0xFFFFFFFFu;
-          uint64_t st = id + wbase * GOLDEN;
-          const uint32_t one = *(volatile uint32_t*)&s_one;
-          uint32_t c_lo = 0, c_hi = 0;
-          const uint32_t k4 = a.k4;
-#define MIX mix64
-#include "pm64_body.inc"
-#undef MIX
-          const uint64_t cand = live ? (((uint64_t)c_hi << 32) | c_lo) : 0ULL;
-          // candidates are cheap (1-2 stream words + a compare against the
-          // slot's own minimum) but scattered: a few lanes per warp-step.  They
-          // are queued per warp and checked 32 at a time with every lane busy;
-          // only the all-candidate start (infinite threshold) or a queue
-          // overflow runs them in place.  The threshold refresh is periodic --
-          // a stale, larger tmax only admits more candidates.
-          const bool inf = !(tmax < 1e300);
-          if (use_q) {
-            const int c = __popcll(cand);
-            int x = c;                                   // inclusive lane scan
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const int y = __shfl_up_sync(0xffffffffu, x, o);
-              if (lane >= o) x += y;
-            }
-            const int total = __shfl_sync(0xffffffffu, x, 31);
-            const bool direct = __any_sync(0xffffffffu, inf) || qn + total > PM64_CQ;
-            if (direct) {
-              if (cand) pm64_candidates<EXPO>(cand, id, w, (uint32_t)e, t, tpg, table);
-            } else if (total) {
-              int pos = qn + x - c;
-              for (uint64_t cb = cand; cb; cb &= cb - 1)
-                cq[pos++] = make_uint2((uint32_t)e, ((uint32_t)t << 6) | (uint32_t)(__ffsll((long long)cb) - 1));
-              qn += total;
-              __syncwarp();
-              while (qn >= 32) {
-                qn -= 32;
-                const uint2 en = cq[qn + lane];
-                __syncwarp();
-                pm64_check_entry<EXPO>(en, ids, ws, tpg, table);
-              }
-            }
-          } else if (cand) {
-            pm64_candidates<EXPO>(cand, id, w, (uint32_t)e, t, tpg, table);
-          }
-          if (++since >= PM64_REFRESH || (cand && inf)) {
-            tmax = fmin(pm64_tmax(table, t, tpg), tg);
-            since = 0;
-          }
-          // reconverge: lanes that took the candidate path would otherwise run
-          // the straight-line body out of phase (independent thread scheduling)
-          __syncwarp();
-        }
-        if (use_q && lane < qn) pm64_check_entry<EXPO>(cq[lane], ids, ws, tpg, table);
-      }
-      __syncthreads();
-      // verification: every slot filled and <= tg
-      {
-        unsigned long long mx = 0;
-        for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-          const unsigned long long h = table[k].h;
-          mx = h > mx ? h : mx;
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-          const unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
-          mx = v > mx ? v : mx;
-        }
-        if (threadIdx.x == 0) s_retry = 0;
-        __syncthreads();
-        if ((threadIdx.x & 31) == 0 && __longlong_as_double((long long)mx) > tg) atomicOr(&s_retry, 1);
-        __syncthreads();
-        const int retry = s_retry;
-        __syncthreads();
-        if (!retry || !(tg < 1e300)) break;
-        tg = attempt >= 1 ? inf_d : tg * 4.0;
-      }
-    }
+    pm64_range<EXPO>(a, off, 0, n, table, smem, &s_one, s_wsum, &s_retry);
     uint64_t* sig = a.sig + (size_t)s * m;
     for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
       const unsigned long long bi = table[pm64_slot(k / PM64_C, (int)(k % PM64_C), tpg)].idx;
@@ -447,6 +471,166 @@ __global__ void __launch_bounds__(PMIN_THREADS, PM64_MINBLOCKS) pminhash64_kerne
       a.stats[s * 3 + 2] = 0;
     }
     __syncthreads();
+  }
+}
+
+// ---- large sets split across CTAs ------------------------------------------
+// One CTA per set caps a set's speed at one SM (a 10^6-element set at m = 1024
+// would take ~0.4 s alone).  The largest sets (an LPT-order prefix, n >=
+// split_n) are cut into parts of <= split_n elements; persistent CTAs take
+// parts from a counter, compute each part's exact minima in shared memory
+// (pm64_range) and merge them into the set's global table with 128-bit CAS
+// (lexicographic (h, index): the merge is order-independent), and a final
+// pass writes the ids.
+
+__device__ __forceinline__ void slot_offer_global(Slot* p, unsigned long long h,
+                                                  unsigned long long idx) {
+  unsigned long long ch, ci;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(ch), "=l"(ci) : "l"(p)
+               : "memory");
+  while (h < ch || (h == ch && idx < ci)) {
+    unsigned long long oh, oi;
+    asm volatile(
+        "{\n\t.reg .b128 c, n, d;\n\t"
+        "mov.b128 c, {%2, %3};\n\t"
+        "mov.b128 n, {%4, %5};\n\t"
+        "atom.global.cas.b128 d, [%6], c, n;\n\t"
+        "mov.b128 {%0, %1}, d;\n\t}"
+        : "=l"(oh), "=l"(oi)
+        : "l"(ch), "l"(ci), "l"(h), "l"(idx), "l"(p)
+        : "memory");
+    if (oh == ch && oi == ci) return;
+    ch = oh;
+    ci = oi;
+  }
+}
+
+// single CTA: which sets to split, parts per split set, prefix.  A set is
+// split when it is larger than both split_n and twice its fair share of the
+// GPU (all elements / CTA slots) -- a batch of many mid-size sets keeps the
+// one-CTA path -- i.e. n >= 2^k for the smallest such power of two; with the
+// LPT order by bit length those sets are an order prefix (binary search).
+__global__ void pm64_split_prep_kernel(PMinArgs a, long long cta_slots) {
+  __shared__ long long s_run;
+  __shared__ long long s_warp[32];
+  __shared__ long long s_nsplit;
+  if (threadIdx.x == 0) {
+    const long long total = a.offsets[a.nsets] - a.offsets[0];
+    long long thr = 2 * total / (cta_slots > 0 ? cta_slots : 1);
+    if (thr < a.split_n) thr = a.split_n;
+    long long p2 = 1;
+    while (p2 < thr) p2 <<= 1;
+    long long lo = 0, hi = a.nsets;                 // first order index with n < p2
+    while (lo < hi) {
+      const long long mid = (lo + hi) / 2;
+      const int64_t sm = a.order[mid];
+      if (a.offsets[sm + 1] - a.offsets[sm] >= p2) lo = mid + 1; else hi = mid;
+    }
+    s_nsplit = lo < a.split_cap ? lo : a.split_cap;
+  }
+  __syncthreads();
+  const long long nsplit = s_nsplit;
+  if (threadIdx.x == 0) s_run = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (long long i0 = 0; i0 < nsplit; i0 += blockDim.x) {
+    const long long i = i0 + threadIdx.x;
+    long long parts = 0;
+    if (i < nsplit) {
+      const int64_t s = a.order[i];
+      const int64_t n = a.offsets[s + 1] - a.offsets[s];
+      parts = (n + a.split_n - 1) / a.split_n;
+    }
+    long long x = parts;                          // inclusive block scan
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[wid] = x;
+    __syncthreads();
+    long long before = 0;
+    for (int k = 0; k < wid; k++) before += s_warp[k];
+    long long chunk_total = 0;
+    for (int k = 0; k < nw; k++) chunk_total += s_warp[k];
+    if (i < nsplit) a.part_base[i] = s_run + before + x - parts;
+    __syncthreads();
+    if (threadIdx.x == 0) s_run += chunk_total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    a.part_base[nsplit] = s_run;
+    a.split_info[0] = nsplit;
+    a.split_info[1] = s_run;
+    a.split_info[2] = 0;
+  }
+}
+
+__global__ void pm64_split_init_kernel(PMinArgs a) {
+  const int64_t total = (int64_t)a.split_info[0] * a.m;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    a.gtab[q].h = EMPTY_H;
+    a.gtab[q].idx = EMPTY_IDX;
+  }
+}
+
+template <bool EXPO>
+__global__ void __launch_bounds__(PMIN_THREADS, PM64_MINBLOCKS) pminhash64_split_kernel(PMinArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t m = a.m;
+  const int tpg = (int)(m / PM64_C);
+  Slot* table = reinterpret_cast<Slot*>(smem);
+  __shared__ uint32_t s_one;
+  __shared__ double s_wsum[PMIN_THREADS / 32];
+  __shared__ int s_retry;
+  __shared__ long long s_t;
+  if (threadIdx.x == 0) s_one = 1u;
+  const int64_t nsplit = a.split_info[0];
+  const long long T = a.split_info[1];
+  for (;;) {
+    if (threadIdx.x == 0)
+      s_t = (long long)atomicAdd((unsigned long long*)&a.split_info[2], 1ULL);
+    __syncthreads();
+    const long long t = s_t;
+    if (t >= T) break;
+    int64_t lo = 0, hi = nsplit - 1;               // last i with part_base[i] <= t
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) / 2;
+      if (a.part_base[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    const int64_t i = lo;
+    const int64_t s = a.order[i];
+    const int64_t off = a.offsets[s];
+    const int64_t n = a.offsets[s + 1] - off;
+    const int64_t parts = a.part_base[i + 1] - a.part_base[i];
+    const int64_t p = t - a.part_base[i];
+    const int64_t e0 = n * p / parts, e1 = n * (p + 1) / parts;
+    pm64_range<EXPO>(a, off, e0, e1, table, smem, &s_one, s_wsum, &s_retry);
+    Slot* gt = a.gtab + (size_t)i * m;
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+      const Slot v = table[pm64_slot(k / PM64_C, (int)(k % PM64_C), tpg)];
+      if (v.idx != EMPTY_IDX) slot_offer_global(&gt[k], v.h, v.idx);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void pm64_split_finalize_kernel(PMinArgs a) {
+  const int64_t nsplit = a.split_info[0];
+  const int64_t total = nsplit * a.m;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / a.m, k = q - i * a.m;
+    const int64_t s = a.order[i];
+    const int64_t off = a.offsets[s];
+    const int64_t n = a.offsets[s + 1] - off;
+    const unsigned long long bi = a.gtab[q].idx;
+    a.sig[s * a.m + k] = bi < (unsigned long long)n ? a.ids[off + bi] : 0ULL;
+    if (a.stats && k == 0) {
+      a.stats[s * 3 + 0] = n * a.m;
+      a.stats[s * 3 + 1] = 0;
+      a.stats[s * 3 + 2] = 0;
+    }
   }
 }
 

@@ -70,3 +70,23 @@ def test_random_vs_oracle(algo, dist):
         ref, _ = orc.sketch_csr(algo, m, batch.ids, batch.weights, batch.offsets, threads=8)
         got, _ = _gpu_sig(algo, m, batch)
         assert (got != ref).sum() == 0
+
+
+@pytest.mark.parametrize("split_n,cap", [(256, 1024), (64, 3), (1024, 1)])
+@pytest.mark.parametrize("algo", ["pminhash", "minhash"])
+def test_pminhash_split_sets_vs_oracle(monkeypatch, split_n, cap, algo):
+    """Large sets split across CTAs (partial minima merged with 128-bit global
+    CAS) give the same signatures; with a small cap some large sets stay on
+    the one-CTA path."""
+    from oracle import oracle as orc
+    from paper_1911_00675_b200 import datagen
+    monkeypatch.setenv("PMH_PM64_SPLIT_N", str(split_n))
+    monkeypatch.setenv("PMH_PM64_SPLIT_CAP", str(cap))
+    rng = np.random.default_rng(split_n + cap)
+    sizes = np.concatenate([[5000, 3000, 1], rng.integers(1, 2500, 20)])
+    batch = datagen.random_sets(int(rng.integers(1 << 30)), sizes, "pareto1.5")
+    w = None if algo == "minhash" else batch.weights
+    for m in (64, 1024):
+        ref, _ = orc.sketch_csr(algo, m, batch.ids, w, batch.offsets, threads=8)
+        got, _ = _gpu_sig(algo, m, batch)
+        assert (got != ref).sum() == 0, (algo, m)
