@@ -259,9 +259,7 @@ int get_aux(AuxStream** out, int slot = 0) {
     // from the start instead of as a tail
     int least = 0, greatest = 0;
     PMH_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-    const char* ev = getenv("PMH_AUX_PRIO");
-    const int prio = (ev && ev[0] == '0') ? least : greatest;
-    PMH_CUDA(cudaStreamCreateWithPriority(&a.s, cudaStreamNonBlocking, prio));
+    PMH_CUDA(cudaStreamCreateWithPriority(&a.s, cudaStreamNonBlocking, greatest));
     PMH_CUDA(cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming));
     PMH_CUDA(cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming));
     it = g_aux.emplace(std::make_pair(dev, slot), a).first;
@@ -511,7 +509,7 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
   void* order_ws = ow.mem;
   if (pmin) {
     PMinArgs a{ids, algo == ALG_PMINHASH ? weights : nullptr, offsets, order, nsets, m,
-               sig_out, stats_out, d_err_set, 4u};
+               sig_out, stats_out, d_err_set};
     if (!pm_split) {
       e = algo == ALG_PMINHASH ? launch_pminhash<true>(a, st) : launch_pminhash<false>(a, st);
     } else {
@@ -566,14 +564,8 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
       }
     };
     // the small-set kernel first (see get_aux)
-    static const bool small_first = !(getenv("PMH_SMALL_FIRST") && getenv("PMH_SMALL_FIRST")[0] == '0');
-    if (small_first) {
-      e = small();
-      if (e == cudaSuccess) e = big();
-    } else {
-      e = big();
-      if (e == cudaSuccess) e = small();
-    }
+    e = small();
+    if (e == cudaSuccess) e = big();
     cudaEventRecord(aux->join, aux->s);
     cudaStreamWaitEvent(st, aux->join, 0);
   }

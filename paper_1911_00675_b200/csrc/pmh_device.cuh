@@ -45,23 +45,6 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // K:40-44
   return z ^ (z >> 31);
 }
 
-// mix64 with its first xor-shift moved from the ALU pipe to the FMA pipe:
-// (x >> 30) for 64-bit x = (hi, lo) is lo' = (hi << 2) + umulhi(lo, 4),
-// hi' = umulhi(hi, 4); `k4` must be 4 but arrive at run time (a kernel
-// argument) so ptxas emits IMAD/IMAD.HI instead of folding to LEA/SHF.  Used
-// by the ALU-bound P-MinHash hot loop to balance the ALU and FMA pipes;
-// bit-identical to mix64.
-__device__ __forceinline__ uint64_t mix64_bal(uint64_t x, uint32_t k4) {
-  const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
-  uint32_t t, lo, hi;
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(t) : "r"(xl), "r"(k4));
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(lo) : "r"(xh), "r"(k4), "r"(t));
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi) : "r"(xh), "r"(k4));
-  uint64_t z = ((uint64_t)(xh ^ hi) << 32) | (uint64_t)(xl ^ lo);
-  z *= MIX1;
-  z = (z ^ (z >> 27)) * MIX2;
-  return z ^ (z >> 31);
-}
 
 // word j (1-based) of the stream seeded with `seed`
 __device__ __forceinline__ uint64_t stream_word(uint64_t seed, uint64_t j) {
@@ -135,15 +118,7 @@ __device__ __forceinline__ int64_t uniform_int(Stream& st, int64_t n) {  // K:11
 }
 
 // E = -log1p(-U) given the 53 raw bits (K:120-122)
-#ifndef PMH_EXP1_NOINLINE
-#define PMH_EXP1_NOINLINE 0
-#endif
-#if PMH_EXP1_NOINLINE
-__device__ __noinline__
-#else
-__device__ __forceinline__
-#endif
-double exp1_from_bits(uint64_t b53) {
+__device__ __forceinline__ double exp1_from_bits(uint64_t b53) {
   return -g_log1p(-((double)b53 * INV53));
 }
 

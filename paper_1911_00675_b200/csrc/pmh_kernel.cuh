@@ -14,9 +14,6 @@
 namespace pmh {
 
 constexpr double HEAVY_POINTS = 8.0;   // expected points above which mode B runs
-#ifndef PMH_L2_PREFETCH
-#define PMH_L2_PREFETCH 1
-#endif
 
 // Division-free prefilter for the common case of large sets: decide from the
 // element's first stream word whether its FIRST point exceeds thr and the
@@ -238,10 +235,8 @@ __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS) sketch_sets_
     // arrive there by the sum itself): the element loop then prefetches one
     // chunk ahead from L2 instead of HBM, whose latency that single chunk in
     // flight per warp could not cover.
-#if PMH_L2_PREFETCH
     for (int64_t L = threadIdx.x; L * 16 < n; L += blockDim.x)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(ids + L * 16));
-#endif
     double W;
     if (family_weighted(F) && w) {
       // four independent loads in flight per thread (latency-bound otherwise)

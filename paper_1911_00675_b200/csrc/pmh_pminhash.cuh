@@ -28,7 +28,6 @@ struct PMinArgs {
   uint64_t* sig;
   int64_t* stats;
   long long* err_set;
-  uint32_t k4;              // == 4, opaque to the compiler (see mix64_bal)
   // split large sets (static kernel only; all null/0 when not splitting):
   // order[0, *nsplit) are the split sets, each in parts of <= split_n elements
   const unsigned* big_count;   // device: sets with n >= split_n (an order prefix)
@@ -190,9 +189,6 @@ constexpr int PM64_C = 64;
 #ifndef PM64_REFRESH
 #define PM64_REFRESH 16    // elements between threshold refreshes
 #endif
-#ifndef PM64_USEQ
-#define PM64_USEQ 1        // per-warp candidate queue
-#endif
 #ifndef PM64_TCONST
 #define PM64_TCONST 8.0    // threshold guess (ln m + c) / W
 #endif
@@ -339,7 +335,7 @@ __device__ __forceinline__ void pm64_range(const PMinArgs& a, int64_t off, int64
       int64_t e = ew + gsub;
       // per-warp candidate queue (warp-aligned groups only: the trip count
       // and every lane must be warp-uniform for the collectives)
-      const bool use_q = PM64_USEQ && ((32 % tpg == 0) || (tpg % 32 == 0));
+      const bool use_q = (32 % tpg == 0) || (tpg % 32 == 0);
       const int lane = threadIdx.x & 31;
       uint2* cq = reinterpret_cast<uint2*>(smem + sizeof(Slot) * m) + (threadIdx.x >> 5) * PM64_CQ;
       int qn = 0;
@@ -361,7 +357,6 @@ __device__ __forceinline__ void pm64_range(const PMinArgs& a, int64_t off, int64
         uint64_t st = id + wbase * GOLDEN;
         const uint32_t one = *(volatile uint32_t*)&s_one;
         uint32_t c_lo = 0, c_hi = 0;
-        const uint32_t k4 = a.k4;
 #define MIX mix64
 #include "pm64_body.inc"
 #undef MIX

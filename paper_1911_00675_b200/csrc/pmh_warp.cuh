@@ -351,17 +351,6 @@ __device__ void parse_fy_parallel(const SetCtx& c, WarpScratch& ws, uint64_t id,
   __syncwarp();
 }
 
-// lazy Fisher-Yates steps (K:222-235) for points i0 .. i0+q-1: r -> label
-__device__ __forceinline__ void fy_steps(WarpScratch& ws, EpochFY fy, int64_t i0, uint32_t q) {
-  for (uint32_t k = 0; k < q; k++) {
-    const int32_t pt = (int32_t)(i0 + k);
-    const int32_t j = pt + ws.lab[k];
-    const int32_t kj = fy.get(j);
-    fy.set(j, fy.get(pt));
-    ws.lab[k] = kj;
-  }
-}
-
 // Warp-parallel lazy Fisher-Yates for the q points of a batch (lane k =
 // point pt_k = i0 + k with index j_k = pt_k + r_k, K:222-235).  Sequentially:
 //   out_k = P[j_k];  P[j_k] = P[pt_k]
