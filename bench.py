@@ -461,10 +461,10 @@ def main():
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "pmh_sketch_csr_host_multi_async, batches pipelined %d deep" % E2E_DEPTH,
                 "sync_call_value": len(variants) * n_total / e2e_sync_s},
-        # per variant call: 3 ordering kernels + for P-MinHash split-prep,
-        # table init, split kernel, regular kernel, finalize (8); for the
-        # ProbMinHash families the set kernel + the small-set kernel (5)
-        "gpu_launches": args.steps * sum(8 if v == "pminhash" else 5 for v in variants),
+        # per variant call: 3 ordering kernels + split prep, table init, split
+        # kernel, finalize + the one-CTA-per-set kernel (8); the ProbMinHash
+        # families also launch their small-set kernel (9)
+        "gpu_launches": args.steps * sum(8 if v == "pminhash" else 9 for v in variants),
         "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),

@@ -268,26 +268,49 @@ int get_aux(AuxStream** out, int slot = 0) {
   return PMH_OK;
 }
 
-// P-MinHash with its largest sets split across CTAs: prep (part counts) and
-// table init on `st`, then the split kernel on `st` beside the regular kernel
-// (remaining sets) on the auxiliary stream, then the ids of the split sets.
+// Split workspace for the largest sets (pmh_split.cuh): slot table, part
+// prefix and counters, from the stream-ordered pool.
+struct SplitWs {
+  SplitArgs sp{};
+  char* mem = nullptr;
+};
+cudaError_t split_setup(const int64_t* offsets, const int32_t* order, int64_t nsets, int64_t c_off,
+                        int64_t split_n, int64_t split_cap, int64_t m, int64_t* stats,
+                        long long cta_slots, cudaStream_t st, SplitWs* ws) {
+  const size_t bt = sizeof(Slot) * (size_t)split_cap * (size_t)m;
+  const size_t bp = sizeof(int64_t) * (size_t)(split_cap + 1);
+  cudaError_t e = cudaMallocAsync((void**)&ws->mem, bt + bp + 4 * sizeof(long long), st);
+  if (e != cudaSuccess) return e;
+  SplitArgs& sp = ws->sp;
+  sp.offsets = offsets;
+  sp.order = order;
+  sp.nsets = nsets;
+  sp.c_off = c_off;
+  sp.split_n = split_n;
+  sp.split_cap = split_cap;
+  sp.m = m;
+  sp.gtab = reinterpret_cast<Slot*>(ws->mem);
+  sp.part_base = reinterpret_cast<int64_t*>(ws->mem + bt);
+  sp.info = reinterpret_cast<long long*>(ws->mem + bt + bp);
+  sp.stats = stats;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  split_prep_kernel<<<1, 1024, 0, st>>>(sp, cta_slots);
+  split_init_kernel<<<(unsigned)(sms * 4), 256, 0, st>>>(sp);
+  return cudaGetLastError();
+}
+
+// P-MinHash with its largest sets split across CTAs: prep and table init on
+// `st`, then the split kernel on `st` beside the regular kernel (remaining
+// sets) on the auxiliary stream, then the ids of the split sets.
 template <bool EXPO>
-cudaError_t launch_pminhash_split(PMinArgs a, const unsigned* big_count, int64_t split_n,
-                                  int64_t split_cap, cudaStream_t st, int aux_slot) {
+cudaError_t launch_pminhash_split(PMinArgs a, int64_t split_n, int64_t split_cap,
+                                  cudaStream_t st, int aux_slot) {
   AuxStream* aux = nullptr;
   if (get_aux(&aux, aux_slot) != PMH_OK) return cudaErrorUnknown;
-  char* ws = nullptr;
-  const size_t bt = sizeof(Slot) * (size_t)split_cap * (size_t)a.m;
-  const size_t bp = sizeof(int64_t) * (size_t)(split_cap + 1);
-  cudaError_t e = cudaMallocAsync((void**)&ws, bt + bp + 4 * sizeof(long long), st);
-  if (e != cudaSuccess) return e;
-  a.big_count = big_count;
-  a.split_cap = split_cap;
-  a.split_n = split_n;
-  a.gtab = reinterpret_cast<Slot*>(ws);
-  a.part_base = reinterpret_cast<int64_t*>(ws + bt);
-  a.split_info = reinterpret_cast<long long*>(ws + bt + bp);
   const size_t smem = sizeof(Slot) * (size_t)a.m + sizeof(uint2) * PM64_CQ * (PMIN_THREADS / 32);
+  cudaError_t e;
   if ((e = cudaFuncSetAttribute(pminhash64_split_kernel<EXPO>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
     return e;
@@ -297,16 +320,19 @@ cudaError_t launch_pminhash_split(PMinArgs a, const unsigned* big_count, int64_t
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pminhash64_split_kernel<EXPO>,
                                                 PMIN_THREADS, smem);
   if (per_sm < 1) per_sm = 1;
-  pm64_split_prep_kernel<<<1, 1024, 0, st>>>(a, (long long)sms * per_sm);
-  pm64_split_init_kernel<<<(unsigned)(sms * 4), 256, 0, st>>>(a);
+  SplitWs ws;
+  if ((e = split_setup(a.offsets, a.order, a.nsets, 0, split_n, split_cap, a.m, a.stats,
+                       (long long)sms * per_sm, st, &ws)) != cudaSuccess)
+    return e;
+  a.split_info = ws.sp.info;
   PMH_CUDA_E(cudaEventRecord(aux->fork, st));
   PMH_CUDA_E(cudaStreamWaitEvent(aux->s, aux->fork, 0));
   if ((e = launch_pminhash<EXPO>(a, aux->s)) != cudaSuccess) return e;   // remaining sets
-  pminhash64_split_kernel<EXPO><<<(unsigned)(sms * per_sm), PMIN_THREADS, smem, st>>>(a);
-  pm64_split_finalize_kernel<<<(unsigned)(sms * 4), 256, 0, st>>>(a);
+  pminhash64_split_kernel<EXPO><<<(unsigned)(sms * per_sm), PMIN_THREADS, smem, st>>>(a, ws.sp);
+  split_finalize_kernel<<<(unsigned)(sms * 4), 256, 0, st>>>(ws.sp, a.ids, a.sig);
   PMH_CUDA_E(cudaEventRecord(aux->join, aux->s));
   PMH_CUDA_E(cudaStreamWaitEvent(st, aux->join, 0));
-  cudaFreeAsync(ws, st);
+  cudaFreeAsync(ws.mem, st);
   return cudaGetLastError();
 }
 
@@ -513,10 +539,9 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
     if (!pm_split) {
       e = algo == ALG_PMINHASH ? launch_pminhash<true>(a, st) : launch_pminhash<false>(a, st);
     } else {
-      e = algo == ALG_PMINHASH ? launch_pminhash_split<true>(a, ow.counts + 1, split_n, split_cap,
-                                                             st, aux_slot)
-                               : launch_pminhash_split<false>(a, ow.counts + 1, split_n,
-                                                              split_cap, st, aux_slot);
+      e = algo == ALG_PMINHASH
+              ? launch_pminhash_split<true>(a, split_n, split_cap, st, aux_slot)
+              : launch_pminhash_split<false>(a, split_n, split_cap, st, aux_slot);
     }
   } else {
     const Tables* tp = nullptr;
@@ -563,11 +588,50 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
         default: return launch_small<FAM_UW4>(a, aux->s);
       }
     };
+    // the largest sets split across CTAs first (pmh_split.cuh): parts of
+    // split_n elements (each part pays its own coupon phase, ~m ln m points,
+    // so parts are larger than P-MinHash's)
+    SplitWs sws;
+    int64_t sp_n = 131072, sp_cap = 1024;
+    if (const char* ev = getenv("PMH_SPLIT_N")) sp_n = atoll(ev);
+    if (const char* ev = getenv("PMH_SPLIT_CAP")) sp_cap = atoll(ev);
+    if (sp_cap > (1LL << 24) / m) sp_cap = (1LL << 24) / m;
+    auto split = [&]() -> cudaError_t {
+      const size_t smem = sketch_smem_bytes(fam, m, SKETCH_THREADS);
+      int dev = 0, sms = 148, per_sm = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      auto go = [&](auto kern) -> cudaError_t {
+        cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem);
+        if (e2 != cudaSuccess) return e2;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SKETCH_THREADS, smem);
+        if (per_sm < 1) per_sm = 1;
+        e2 = split_setup(offsets, order, nsets, (int64_t)(7.0 * (double)m), sp_n, sp_cap, m,
+                         stats_out, (long long)sms * per_sm, st, &sws);
+        if (e2 != cudaSuccess) return e2;
+        a.split_info = sws.sp.info;
+        kern<<<(unsigned)(sms * per_sm), SKETCH_THREADS, smem, st>>>(a, sws.sp);
+        split_finalize_kernel<<<(unsigned)(sms * 4), 256, 0, st>>>(sws.sp, ids, sig_out);
+        return cudaGetLastError();
+      };
+      switch (fam) {
+        case FAM_PMH1: return go(sketch_split_kernel<FAM_PMH1>);
+        case FAM_PMH2: return go(sketch_split_kernel<FAM_PMH2>);
+        case FAM_PMH3: return go(sketch_split_kernel<FAM_PMH3>);
+        case FAM_PMH4: return go(sketch_split_kernel<FAM_PMH4>);
+        case FAM_UW3: return go(sketch_split_kernel<FAM_UW3>);
+        default: return go(sketch_split_kernel<FAM_UW4>);
+      }
+    };
+    const bool do_split = sp_n >= 64 && sp_cap > 0;
     // the small-set kernel first (see get_aux)
     e = small();
+    if (e == cudaSuccess && do_split) e = split();
     if (e == cudaSuccess) e = big();
     cudaEventRecord(aux->join, aux->s);
     cudaStreamWaitEvent(st, aux->join, 0);
+    if (sws.mem) cudaFreeAsync(sws.mem, st);
   }
   cudaFreeAsync(order_ws, st);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");

@@ -10,6 +10,7 @@
 // threshold guess t exact-safe (retry with a larger t otherwise).
 #pragma once
 #include "pmh_warp.cuh"
+#include "pmh_split.cuh"
 
 namespace pmh {
 
@@ -183,40 +184,148 @@ __device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const 
   if (0.0 > c.tprev) c.points += rej;          // rejected first points
 }
 
+// per-CTA shared state of one set (or one part of a split set)
+struct SetShared {
+  unsigned long long hmax;
+  unsigned int filled;
+  unsigned int next;
+  int retry;
+  double red[32];
+  long long redl[32];
+};
+
+// The verified minima of elements [e0, e1) of the set at `off` in the shared
+// slot table (in-set element indices); the threshold guess uses the range's
+// own total weight.  Returns true if an element hit a loop cap.  Counters of
+// the range in pts/mul/upd (CTA-reduced, valid in every thread).
+template <int F>
+__device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, int64_t e0,
+                                             int64_t e1, Slot* slots, WarpScratch* wscr,
+                                             uint32_t* fy_dense, bool warp_ok, SetShared& sh,
+                                             long long* pts, long long* mul, long long* upd) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const int64_t m = a.m;
+  const int64_t n = e1 - e0;
+  const uint64_t* ids = a.ids + off + e0;
+  const double* w = a.w ? a.w + off + e0 : nullptr;
+  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+    slots[k].h = EMPTY_H;
+    slots[k].idx = EMPTY_IDX;
+  }
+  // Pull the range's ids into L2 while the weights are summed (the weights
+  // arrive there by the sum itself): the element loop then reads its chunks
+  // from L2 instead of HBM.
+  for (int64_t L = threadIdx.x; L * 16 < n; L += blockDim.x)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(ids + L * 16));
+  double W;
+  if (family_weighted(F) && w) {
+    // four independent loads in flight per thread (latency-bound otherwise)
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+    const int64_t B = blockDim.x;
+    int64_t e = threadIdx.x;
+    for (; e + 3 * B < n; e += 4 * B) {
+      p0 += __ldg(&w[e]);
+      p1 += __ldg(&w[e + B]);
+      p2 += __ldg(&w[e + 2 * B]);
+      p3 += __ldg(&w[e + 3 * B]);
+    }
+    for (; e < n; e += B) p0 += __ldg(&w[e]);
+    W = block_sum((p0 + p1) + (p2 + p3), sh.red);
+  } else {
+    W = (double)n;
+  }
+  if (threadIdx.x == 0) { sh.hmax = EMPTY_H; sh.filled = 0; }
+
+  SetCtx c;
+  c.slots = slots;
+  c.hmax_bits = &sh.hmax;
+  c.filled = &sh.filled;
+  c.m = m;
+  c.kbits = bits_for(m);
+  c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
+  c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
+  c.eoff = e0;
+  double tg = (double)m * (log((double)m) + a.tconst) / W;
+  if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
+  bool failed = false;
+  int64_t chunk = (n + 2 * nwarps - 1) / (2 * nwarps);
+  chunk = chunk < 1 ? 1 : (chunk > 32 * PMH_EPL ? 32 * PMH_EPL : chunk);
+
+  for (int attempt = 0;; attempt++) {
+    c.tguess = tg;
+    if (threadIdx.x == 0) sh.next = 0;
+    __syncthreads();
+    SharedGrab grab{&sh.next, (unsigned)chunk};
+    warp_elements<F>(c, a.T, ids, w, n, chunk, grab, wscr, fy_dense, warp_ok, failed, lane);
+    __syncthreads();
+    // verification: every slot non-empty and <= tguess
+    unsigned long long mx = 0;
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+      unsigned long long h = slots[k].h;
+      mx = h > mx ? h : mx;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
+      mx = v > mx ? v : mx;
+    }
+    if (threadIdx.x == 0) sh.retry = 0;
+    __syncthreads();
+    if (lane == 0 && __longlong_as_double((long long)mx) > tg) atomicOr(&sh.retry, 1);
+    const int any_fail = __syncthreads_or(failed ? 1 : 0);
+    if (any_fail) { failed = true; break; }
+    if (!sh.retry) break;
+    c.tprev = tg;
+    tg = attempt >= 2 ? __longlong_as_double(0x7FF0000000000000LL) : tg * 4.0;
+    __syncthreads();
+  }
+  if (a.stats) {
+    *pts = block_sum_ll(c.points, sh.redl);
+    *mul = block_sum_ll(c.multi, sh.redl);
+    *upd = block_sum_ll(c.updates, sh.redl);
+  }
+  return failed;
+}
+
 // Dynamic shared memory: Slot[m] | WarpScratch[nwarps] | int32 FY[nwarps][m+1]
 #ifndef SKETCH_MINBLOCKS
 #define SKETCH_MINBLOCKS 3   // 80 registers, 3 CTAs/SM: measured 3-12% faster than 2
 #endif
+
+template <int F>
+__device__ __forceinline__ void sketch_cta_setup(unsigned char* smem, int64_t m, Slot** slots,
+                                                 WarpScratch** wscr, uint32_t** fy_dense) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  *slots = reinterpret_cast<Slot*>(smem);
+  *wscr = reinterpret_cast<WarpScratch*>(smem + sizeof(Slot) * m) + wid;
+  *fy_dense = reinterpret_cast<uint32_t*>(smem + sizeof(Slot) * m + sizeof(WarpScratch) * nwarps) +
+              (size_t)wid * (m + 1);
+  if (family_uses_fy(F)) {  // epoch 0 never matches: the map starts empty
+    for (int64_t p = lane; p <= m; p += 32) (*fy_dense)[p] = 0;
+    if (lane == 0) (*wscr)->epoch = 0;
+  }
+}
+
 template <int F>
 __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS) sketch_sets_kernel(SketchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ unsigned long long s_hmax;
-  __shared__ unsigned int s_filled;
-  __shared__ unsigned int s_next;
-  __shared__ int s_retry;
-  __shared__ double s_red[32];
-  __shared__ long long s_redl[32];
-
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
+  __shared__ SetShared sh;
   const int64_t m = a.m;
-  Slot* slots = reinterpret_cast<Slot*>(smem);
-  WarpScratch* wscr = reinterpret_cast<WarpScratch*>(smem + sizeof(Slot) * m) + wid;
-  uint32_t* fy_dense = reinterpret_cast<uint32_t*>(
-                           smem + sizeof(Slot) * m + sizeof(WarpScratch) * nwarps) +
-                       (size_t)wid * (m + 1);
-  if (family_uses_fy(F)) {  // epoch 0 never matches: the map starts empty
-    for (int64_t p = lane; p <= m; p += 32) fy_dense[p] = 0;
-    if (lane == 0) wscr->epoch = 0;
-  }
+  Slot* slots;
+  WarpScratch* wscr;
+  uint32_t* fy_dense;
+  sketch_cta_setup<F>(smem, m, &slots, &wscr, &fy_dense);
   // mode B needs static point offsets (power-of-two m) unless the family
   // parses its bit offsets (Fisher-Yates families)
   const bool warp_ok = family_uses_fy(F) || ((m & (m - 1)) == 0);
 
   // with a small-set kernel running beside it, this kernel takes the large
-  // sets only: the prefix order[0, counts[0]) of the LPT order
+  // sets only: the prefix order[0, counts[0]) of the LPT order, minus the
+  // split sets at its front
   const int64_t n_mine = a.counts ? (int64_t)a.counts[0] : a.nsets;
-  for (int64_t bs = blockIdx.x; bs < n_mine; bs += gridDim.x) {
+  const int64_t first = a.split_info ? (int64_t)a.split_info[0] : 0;
+  for (int64_t bs = first + blockIdx.x; bs < n_mine; bs += gridDim.x) {
     const int64_t s = a.order ? (int64_t)a.order[bs] : bs;
     const int64_t off = a.offsets[s];
     const int64_t n = a.offsets[s + 1] - off;
@@ -224,99 +333,60 @@ __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS) sketch_sets_
       if (threadIdx.x == 0) atomicMin(a.err_set, (long long)s);
       continue;
     }
-    const uint64_t* ids = a.ids + off;
-    const double* w = a.w ? a.w + off : nullptr;
-
-    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-      slots[k].h = EMPTY_H;
-      slots[k].idx = EMPTY_IDX;
-    }
-    // Pull the set's ids into L2 while the weights are summed (the weights
-    // arrive there by the sum itself): the element loop then prefetches one
-    // chunk ahead from L2 instead of HBM, whose latency that single chunk in
-    // flight per warp could not cover.
-    for (int64_t L = threadIdx.x; L * 16 < n; L += blockDim.x)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(ids + L * 16));
-    double W;
-    if (family_weighted(F) && w) {
-      // four independent loads in flight per thread (latency-bound otherwise)
-      double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-      const int64_t B = blockDim.x;
-      int64_t e = threadIdx.x;
-      for (; e + 3 * B < n; e += 4 * B) {
-        p0 += __ldg(&w[e]);
-        p1 += __ldg(&w[e + B]);
-        p2 += __ldg(&w[e + 2 * B]);
-        p3 += __ldg(&w[e + 3 * B]);
-      }
-      for (; e < n; e += B) p0 += __ldg(&w[e]);
-      W = block_sum((p0 + p1) + (p2 + p3), s_red);
-    } else {
-      W = (double)n;
-    }
-    if (threadIdx.x == 0) { s_hmax = EMPTY_H; s_filled = 0; }
-
-    SetCtx c;
-    c.slots = slots;
-    c.hmax_bits = &s_hmax;
-    c.filled = &s_filled;
-    c.m = m;
-    c.kbits = bits_for(m);
-    c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
-    c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
-    double tg = (double)m * (log((double)m) + a.tconst) / W;
-    if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
-    bool failed = false;
-    int64_t chunk = (n + 2 * nwarps - 1) / (2 * nwarps);
-    chunk = chunk < 1 ? 1 : (chunk > 32 * PMH_EPL ? 32 * PMH_EPL : chunk);
-
-    for (int attempt = 0;; attempt++) {
-      c.tguess = tg;
-      if (threadIdx.x == 0) s_next = 0;
-      __syncthreads();
-      SharedGrab grab{&s_next, (unsigned)chunk};
-      warp_elements<F>(c, a.T, ids, w, n, chunk, grab, wscr, fy_dense, warp_ok, failed, lane);
-      __syncthreads();
-      // verification: every slot non-empty and <= tguess
-      unsigned long long mx = 0;
-      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-        unsigned long long h = slots[k].h;
-        mx = h > mx ? h : mx;
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
-        mx = v > mx ? v : mx;
-      }
-      if (threadIdx.x == 0) s_retry = 0;
-      __syncthreads();
-      if (lane == 0 && __longlong_as_double((long long)mx) > tg) atomicOr(&s_retry, 1);
-      const int any_fail = __syncthreads_or(failed ? 1 : 0);
-      if (any_fail) { failed = true; break; }
-      if (!s_retry) break;
-      c.tprev = tg;
-      tg = attempt >= 2 ? __longlong_as_double(0x7FF0000000000000LL) : tg * 4.0;
-      __syncthreads();
-    }
-    if (failed) {
-      if (threadIdx.x == 0) {
-        atomicOr(a.err_flags, (unsigned long long)ERRF_RANDOMNESS);
-        atomicMin(a.err_set, (long long)s);
-      }
+    long long pts = 0, mul = 0, upd = 0;
+    const bool failed = sketch_range<F>(a, off, 0, n, slots, wscr, fy_dense, warp_ok, sh, &pts,
+                                        &mul, &upd);
+    if (failed && threadIdx.x == 0) {
+      atomicOr(a.err_flags, (unsigned long long)ERRF_RANDOMNESS);
+      atomicMin(a.err_set, (long long)s);
     }
     uint64_t* sig = a.sig + (size_t)s * m;
+    const uint64_t* ids = a.ids + off;
     for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
       const unsigned long long ix = slots[k].idx;
       sig[k] = ix < (unsigned long long)n ? ids[ix] : 0ULL;
     }
-    if (a.stats) {
-      long long pts = block_sum_ll(c.points, s_redl);
-      long long mul = block_sum_ll(c.multi, s_redl);
-      long long upd = block_sum_ll(c.updates, s_redl);
-      if (threadIdx.x == 0) {
-        a.stats[s * 3 + 0] = pts;
-        a.stats[s * 3 + 1] = mul;
-        a.stats[s * 3 + 2] = upd;
-      }
+    if (a.stats && threadIdx.x == 0) {
+      a.stats[s * 3 + 0] = pts;
+      a.stats[s * 3 + 1] = mul;
+      a.stats[s * 3 + 2] = upd;
+    }
+    __syncthreads();
+  }
+}
+
+// Parts of the split sets (pmh_split.cuh): persistent CTAs, each part's
+// verified minima merged into the set's global table.
+template <int F>
+__global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS)
+    sketch_split_kernel(SketchArgs a, SplitArgs sp) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ SetShared sh;
+  __shared__ long long s_t;
+  const int64_t m = a.m;
+  Slot* slots;
+  WarpScratch* wscr;
+  uint32_t* fy_dense;
+  sketch_cta_setup<F>(smem, m, &slots, &wscr, &fy_dense);
+  const bool warp_ok = family_uses_fy(F) || ((m & (m - 1)) == 0);
+  SplitPart p;
+  while (split_next_part(sp, &s_t, &p)) {
+    long long pts = 0, mul = 0, upd = 0;
+    const bool failed = sketch_range<F>(a, p.off, p.e0, p.e1, slots, wscr, fy_dense, warp_ok, sh,
+                                        &pts, &mul, &upd);
+    if (failed && threadIdx.x == 0) {
+      atomicOr(a.err_flags, (unsigned long long)ERRF_RANDOMNESS);
+      atomicMin(a.err_set, (long long)p.s);
+    }
+    Slot* gt = sp.gtab + (size_t)p.i * m;
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+      const Slot v = slots[k];
+      if (v.idx != EMPTY_IDX) slot_offer_global(&gt[k], v.h, v.idx);
+    }
+    if (a.stats && threadIdx.x == 0) {
+      atomicAdd((unsigned long long*)&a.stats[p.s * 3 + 0], (unsigned long long)pts);
+      atomicAdd((unsigned long long*)&a.stats[p.s * 3 + 1], (unsigned long long)mul);
+      atomicAdd((unsigned long long*)&a.stats[p.s * 3 + 2], (unsigned long long)upd);
     }
     __syncthreads();
   }
@@ -407,6 +477,7 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
     c.kbits = bits_for(m);
     c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
     c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
+    c.eoff = 0;
     double tg = (double)m * (log((double)m) + a.tconst) / W;
     if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
     bool failed = false;

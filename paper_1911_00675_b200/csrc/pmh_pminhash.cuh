@@ -15,6 +15,7 @@
 #include <stdint.h>
 
 #include "pmh_device.cuh"
+#include "pmh_split.cuh"
 
 namespace pmh {
 
@@ -28,14 +29,9 @@ struct PMinArgs {
   uint64_t* sig;
   int64_t* stats;
   long long* err_set;
-  // split large sets (static kernel only; all null/0 when not splitting):
-  // order[0, *nsplit) are the split sets, each in parts of <= split_n elements
-  const unsigned* big_count;   // device: sets with n >= split_n (an order prefix)
-  int64_t split_cap;           // at most this many sets are split (gtab rows)
-  int64_t split_n;
-  Slot* gtab;                  // [split_cap, m] merged minima of the split sets
-  int64_t* part_base;          // [split_cap + 1] prefix of parts per split set
-  long long* split_info;       // [0] = nsplit, [1] = total parts, [2] = work counter
+  // order[0, split_info[0]) are split across CTAs (pmh_split.cuh) and skipped
+  // by the one-CTA-per-set kernel; nullptr: no split
+  const long long* split_info;
 };
 
 constexpr int PMIN_THREADS = 256;
@@ -478,99 +474,9 @@ __global__ void __launch_bounds__(PMIN_THREADS, PM64_MINBLOCKS) pminhash64_kerne
 // (lexicographic (h, index): the merge is order-independent), and a final
 // pass writes the ids.
 
-__device__ __forceinline__ void slot_offer_global(Slot* p, unsigned long long h,
-                                                  unsigned long long idx) {
-  unsigned long long ch, ci;
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(ch), "=l"(ci) : "l"(p)
-               : "memory");
-  while (h < ch || (h == ch && idx < ci)) {
-    unsigned long long oh, oi;
-    asm volatile(
-        "{\n\t.reg .b128 c, n, d;\n\t"
-        "mov.b128 c, {%2, %3};\n\t"
-        "mov.b128 n, {%4, %5};\n\t"
-        "atom.global.cas.b128 d, [%6], c, n;\n\t"
-        "mov.b128 {%0, %1}, d;\n\t}"
-        : "=l"(oh), "=l"(oi)
-        : "l"(ch), "l"(ci), "l"(h), "l"(idx), "l"(p)
-        : "memory");
-    if (oh == ch && oi == ci) return;
-    ch = oh;
-    ci = oi;
-  }
-}
-
-// single CTA: which sets to split, parts per split set, prefix.  A set is
-// split when it is larger than both split_n and twice its fair share of the
-// GPU (all elements / CTA slots) -- a batch of many mid-size sets keeps the
-// one-CTA path -- i.e. n >= 2^k for the smallest such power of two; with the
-// LPT order by bit length those sets are an order prefix (binary search).
-__global__ void pm64_split_prep_kernel(PMinArgs a, long long cta_slots) {
-  __shared__ long long s_run;
-  __shared__ long long s_warp[32];
-  __shared__ long long s_nsplit;
-  if (threadIdx.x == 0) {
-    const long long total = a.offsets[a.nsets] - a.offsets[0];
-    long long thr = 2 * total / (cta_slots > 0 ? cta_slots : 1);
-    if (thr < a.split_n) thr = a.split_n;
-    long long p2 = 1;
-    while (p2 < thr) p2 <<= 1;
-    long long lo = 0, hi = a.nsets;                 // first order index with n < p2
-    while (lo < hi) {
-      const long long mid = (lo + hi) / 2;
-      const int64_t sm = a.order[mid];
-      if (a.offsets[sm + 1] - a.offsets[sm] >= p2) lo = mid + 1; else hi = mid;
-    }
-    s_nsplit = lo < a.split_cap ? lo : a.split_cap;
-  }
-  __syncthreads();
-  const long long nsplit = s_nsplit;
-  if (threadIdx.x == 0) s_run = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (long long i0 = 0; i0 < nsplit; i0 += blockDim.x) {
-    const long long i = i0 + threadIdx.x;
-    long long parts = 0;
-    if (i < nsplit) {
-      const int64_t s = a.order[i];
-      const int64_t n = a.offsets[s + 1] - a.offsets[s];
-      parts = (n + a.split_n - 1) / a.split_n;
-    }
-    long long x = parts;                          // inclusive block scan
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) s_warp[wid] = x;
-    __syncthreads();
-    long long before = 0;
-    for (int k = 0; k < wid; k++) before += s_warp[k];
-    long long chunk_total = 0;
-    for (int k = 0; k < nw; k++) chunk_total += s_warp[k];
-    if (i < nsplit) a.part_base[i] = s_run + before + x - parts;
-    __syncthreads();
-    if (threadIdx.x == 0) s_run += chunk_total;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    a.part_base[nsplit] = s_run;
-    a.split_info[0] = nsplit;
-    a.split_info[1] = s_run;
-    a.split_info[2] = 0;
-  }
-}
-
-__global__ void pm64_split_init_kernel(PMinArgs a) {
-  const int64_t total = (int64_t)a.split_info[0] * a.m;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    a.gtab[q].h = EMPTY_H;
-    a.gtab[q].idx = EMPTY_IDX;
-  }
-}
-
 template <bool EXPO>
-__global__ void __launch_bounds__(PMIN_THREADS, PM64_MINBLOCKS) pminhash64_split_kernel(PMinArgs a) {
+__global__ void __launch_bounds__(PMIN_THREADS, PM64_MINBLOCKS)
+    pminhash64_split_kernel(PMinArgs a, SplitArgs sp) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int64_t m = a.m;
   const int tpg = (int)(m / PM64_C);
@@ -580,52 +486,17 @@ __global__ void __launch_bounds__(PMIN_THREADS, PM64_MINBLOCKS) pminhash64_split
   __shared__ int s_retry;
   __shared__ long long s_t;
   if (threadIdx.x == 0) s_one = 1u;
-  const int64_t nsplit = a.split_info[0];
-  const long long T = a.split_info[1];
-  for (;;) {
-    if (threadIdx.x == 0)
-      s_t = (long long)atomicAdd((unsigned long long*)&a.split_info[2], 1ULL);
-    __syncthreads();
-    const long long t = s_t;
-    if (t >= T) break;
-    int64_t lo = 0, hi = nsplit - 1;               // last i with part_base[i] <= t
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) / 2;
-      if (a.part_base[mid] <= t) lo = mid; else hi = mid - 1;
-    }
-    const int64_t i = lo;
-    const int64_t s = a.order[i];
-    const int64_t off = a.offsets[s];
-    const int64_t n = a.offsets[s + 1] - off;
-    const int64_t parts = a.part_base[i + 1] - a.part_base[i];
-    const int64_t p = t - a.part_base[i];
-    const int64_t e0 = n * p / parts, e1 = n * (p + 1) / parts;
-    pm64_range<EXPO>(a, off, e0, e1, table, smem, &s_one, s_wsum, &s_retry);
-    Slot* gt = a.gtab + (size_t)i * m;
+  SplitPart p;
+  while (split_next_part(sp, &s_t, &p)) {
+    pm64_range<EXPO>(a, p.off, p.e0, p.e1, table, smem, &s_one, s_wsum, &s_retry);
+    Slot* gt = sp.gtab + (size_t)p.i * m;
     for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
       const Slot v = table[pm64_slot(k / PM64_C, (int)(k % PM64_C), tpg)];
       if (v.idx != EMPTY_IDX) slot_offer_global(&gt[k], v.h, v.idx);
     }
+    if (a.stats && threadIdx.x == 0)
+      atomicAdd((unsigned long long*)&a.stats[p.s * 3], (unsigned long long)((p.e1 - p.e0) * m));
     __syncthreads();
-  }
-}
-
-__global__ void pm64_split_finalize_kernel(PMinArgs a) {
-  const int64_t nsplit = a.split_info[0];
-  const int64_t total = nsplit * a.m;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = q / a.m, k = q - i * a.m;
-    const int64_t s = a.order[i];
-    const int64_t off = a.offsets[s];
-    const int64_t n = a.offsets[s + 1] - off;
-    const unsigned long long bi = a.gtab[q].idx;
-    a.sig[s * a.m + k] = bi < (unsigned long long)n ? a.ids[off + bi] : 0ULL;
-    if (a.stats && k == 0) {
-      a.stats[s * 3 + 0] = n * a.m;
-      a.stats[s * 3 + 1] = 0;
-      a.stats[s * 3 + 2] = 0;
-    }
   }
 }
 

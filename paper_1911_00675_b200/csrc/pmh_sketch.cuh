@@ -51,6 +51,7 @@ struct SetCtx {
   int64_t updates;
   int64_t multi;                     // elements that produced > 1 point
   int since_refresh;                 // batches since the last h_max refresh
+  int64_t eoff;                      // in-set index of element 0 (a split set's part)
 };
 
 __device__ __forceinline__ double ctx_thr(const SetCtx& c) {
@@ -71,7 +72,7 @@ __device__ __noinline__ void hmax_recompute_serial(SetCtx& c) {
 
 __device__ __forceinline__ void ctx_offer(SetCtx& c, int64_t k0, double x,
                                           int64_t e) {
-  unsigned long long prev = slot_offer(&c.slots[k0], x, (unsigned long long)e);
+  unsigned long long prev = slot_offer(&c.slots[k0], x, (unsigned long long)(e + c.eoff));
   if (prev == ~0ULL) return;
   c.updates++;
   if (prev == EMPTY_H) {
@@ -349,6 +350,7 @@ struct SketchArgs {
   Tables T;
   double tconst;            // threshold-guess constant (ln m + tconst)
   const unsigned* counts;   // device: [0] = number of large sets (order prefix)
+  const long long* split_info;  // order[0, split_info[0]) are split (pmh_split.cuh)
 };
 
 __device__ __forceinline__ double block_sum(double v, double* red) {

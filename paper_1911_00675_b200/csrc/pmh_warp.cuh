@@ -77,7 +77,7 @@ __device__ __forceinline__ void win_load(WarpScratch& ws, uint64_t id, uint64_t 
 
 // offer with a refresh trigger instead of an inline serial recompute
 __device__ __forceinline__ bool offer_trig(SetCtx& c, int64_t k0, double x, int64_t e) {
-  unsigned long long prev = slot_offer(&c.slots[k0], x, (unsigned long long)e);
+  unsigned long long prev = slot_offer(&c.slots[k0], x, (unsigned long long)(e + c.eoff));
   if (prev == ~0ULL) return false;
   c.updates++;
   if (prev == EMPTY_H) {

@@ -90,3 +90,23 @@ def test_pminhash_split_sets_vs_oracle(monkeypatch, split_n, cap, algo):
         ref, _ = orc.sketch_csr(algo, m, batch.ids, w, batch.offsets, threads=8)
         got, _ = _gpu_sig(algo, m, batch)
         assert (got != ref).sum() == 0, (algo, m)
+
+
+@pytest.mark.parametrize("cap", [1024, 2])
+@pytest.mark.parametrize("algo", ["probminhash1", "probminhash2", "probminhash3", "probminhash4",
+                                  "probminhash1a", "unweighted3", "unweighted4"])
+def test_probminhash_split_sets_vs_oracle(monkeypatch, cap, algo):
+    """ProbMinHash families with large sets split across CTAs (each part its
+    own verified threshold, merged by 128-bit global CAS) == the oracle."""
+    from oracle import oracle as orc
+    from paper_1911_00675_b200 import datagen
+    monkeypatch.setenv("PMH_SPLIT_N", "64")
+    monkeypatch.setenv("PMH_SPLIT_CAP", str(cap))
+    rng = np.random.default_rng(cap + len(algo))
+    sizes = np.concatenate([[6000, 2500, 1, 2], rng.integers(1, 3000, 16)])
+    batch = datagen.random_sets(int(rng.integers(1 << 30)), sizes, "pareto1.5")
+    w = None if algo.startswith("unweighted") else batch.weights
+    for m in (64, 1024):
+        ref, _ = orc.sketch_csr(algo, m, batch.ids, w, batch.offsets, threads=8)
+        got, _ = _gpu_sig(algo, m, batch)
+        assert (got != ref).sum() == 0, (algo, m)
