@@ -3,12 +3,13 @@
 // Every sketch kernel runs one CTA per set, which caps one set at one SM: a
 // single 10^6-element set (P-MinHash, m = 1024) or 10^7-element set
 // (ProbMinHash) takes tens to hundreds of ms where the whole GPU would take
-// one.  Sets larger than both `split_n` and twice their fair share of the GPU
-// (the batch's total cost / CTA slots) are cut into parts of <= split_n
-// elements.  A part's CTA computes the exact minima of its element range in
-// shared memory -- its own threshold guess, verified, so any range is
-// exact-safe -- and merges them into the set's global slot table with 128-bit
-// CAS on (h, in-set index): lexicographic, hence order-independent.  A final
+// one.  Sets larger than both `split_n` and the batch's fair share per CTA
+// slot (total cost / CTA slots, rounded down to a power of two) are cut into
+// parts of <= split_n elements.  A part's CTA computes the exact minima of
+// its element range in shared memory -- its own threshold guess, verified, so
+// any range is exact-safe -- and merges them into the set's global slot table
+// with 128-bit CAS on (h, in-set index): lexicographic, hence
+// order-independent.  A final
 // pass writes the ids.  Which sets are split is decided on the device (no
 // host sync): the LPT order is by bit length of (n + c), so the sets with
 // n + c >= 2^k form an order prefix, found by binary search.
@@ -24,7 +25,7 @@ struct SplitArgs {
   const int32_t* order;
   int64_t nsets;
   int64_t c_off;          // the order's cost offset (0 for P-MinHash, 7m otherwise)
-  int64_t split_n;        // part size; a set needs n + c_off >= 2 split_n at least
+  int64_t split_n;        // part size; only sets with n >= split_n are split
   int64_t split_cap;      // at most this many sets are split (gtab rows)
   int64_t m;
   Slot* gtab;             // [split_cap, m]
@@ -62,11 +63,14 @@ __global__ void split_prep_kernel(SplitArgs a, long long cta_slots) {
   __shared__ long long s_warp[32];
   __shared__ long long s_nsplit;
   if (threadIdx.x == 0) {
+    // threshold: the largest power of two not above the fair share (total
+    // cost / CTA slots), but at least the smallest power of two >= one part
     const long long total = (a.offsets[a.nsets] - a.offsets[0]) + a.c_off * a.nsets;
-    long long thr = 2 * total / (cta_slots > 0 ? cta_slots : 1);
-    if (thr < a.split_n + a.c_off) thr = a.split_n + a.c_off;
-    long long p2 = 1;
-    while (p2 < thr) p2 <<= 1;
+    const long long fair = total / (cta_slots > 0 ? cta_slots : 1);
+    long long floor_p2 = 1;
+    while (floor_p2 < a.split_n + a.c_off) floor_p2 <<= 1;
+    long long p2 = floor_p2;
+    while (p2 * 2 <= fair) p2 <<= 1;
     long long lo = 0, hi = a.nsets;                 // first order index with n + c < p2
     while (lo < hi) {
       const long long mid = (lo + hi) / 2;
