@@ -116,3 +116,47 @@ def test_gpu_timing_experiment_rows():
         ("pminhash", 64, 1000)]
     assert all(r.mean_ns > 0 for r in rows)
     assert H.timing_csv(rows).count("\n") == 5
+
+
+def test_gpu_unweighted2_statistically_equivalent_to_minhash():
+    """uw2 and MinHash estimate the same J: pooled match fractions agree
+    (two-proportion z-test, the reference's test_sketch.py band)."""
+    wa = np.array([1.0] * 6 + [0.0] * 2)
+    wb = np.array([1.0] * 4 + [0.0, 0.0, 1.0, 1.0])
+    m, s = 64, 4000
+    ma = H.mse_cell_matches(H.ALGORITHM_IDS["unweighted2"], m, wa, wb, 5, s)
+    mb = H.mse_cell_matches(H.ALGORITHM_IDS["minhash"], m, wa, wb, 6, s)
+    pa, pb = ma.mean() / m, mb.mean() / m
+    var = (ma / m).var() / s + (mb / m).var() / s
+    assert abs(pa - pb) / math.sqrt(var) < Z_BAND
+
+
+def test_gpu_criterion_11_bbit_calibration():
+    """test_acceptance.py criterion 11: the b-bit estimator of P-MinHash
+    signatures (m = 4096) is calibrated -- mean estimate within 0.01 of J_P
+    for b = 1, 4, 8 over 2000 pairs of each fixture."""
+    import torch
+    from paper_1911_00675_b200 import sketch_batch
+    from paper_1911_00675_b200.batch import (bbit_device, bbit_estimate, to_device_f64,
+                                             to_device_i64, to_device_u64)
+    from paper_1911_00675_b200.rng import RandomStream
+    m, s = 4096, 2000
+    worst = 0.0
+    for fixture, jp in (("tenth10", 0.1), ("binary8", 0.5), ("ninety10", 0.9)):
+        wa, wb = H.FIXTURES[fixture].arrays()
+        sa_, sb_ = wa > 0, wb > 0
+        st = RandomStream(H.cell_seed(SEED, "bbit", fixture))
+        words = st.u64_batch(s * wa.size).reshape(s, wa.size)
+        ids = np.concatenate([words[:, sa_].ravel(), words[:, sb_].ravel()])
+        w = np.concatenate([np.tile(wa[sa_], s), np.tile(wb[sb_], s)])
+        na, nb = int(sa_.sum()), int(sb_.sum())
+        off = np.concatenate([np.arange(s + 1) * na, s * na + np.arange(1, s + 1) * nb])
+        sig, _ = sketch_batch("pminhash", to_device_u64(ids), to_device_f64(w),
+                              to_device_i64(off.astype(np.int64)), m, want_stats=False)
+        for b in (1, 4, 8):
+            r = bbit_device(sig, b)
+            c = (r[:s] == r[s:]).sum(dim=1).cpu().numpy()
+            worst = max(worst, abs(float(bbit_estimate(c, m, b).mean()) - jp))
+        del sig
+        torch.cuda.empty_cache()
+    assert worst < 0.01, worst
