@@ -8,7 +8,7 @@
 // variant), and early stopping only skips points above the final stop limit
 // H, elements may be processed in ANY order with ANY threshold >= H
 // (SURVEY.md §0 facts 4 and 6).  Each CTA therefore:
-//   1. computes W = sum(w) and a threshold guess t = m (ln m + 4) / W
+//   1. computes W = sum(w) and a threshold guess t = m (ln m + 3) / W
 //      (a point-process estimate of H; correctness never depends on it);
 //   2. streams elements, one per thread, through the variant's exact point
 //      recurrence (Appendix A), skipping every point whose value -- or a
