@@ -14,7 +14,10 @@
 
 namespace pmh {
 
-constexpr double HEAVY_POINTS = 8.0;   // expected points above which mode B runs
+#ifndef PMH_HEAVY_POINTS
+#define PMH_HEAVY_POINTS 16.0   // measured best on config 2 (4 / 6 / 8 / 12 / 16 / 24 / 32 / 48 tried)
+#endif
+constexpr double HEAVY_POINTS = PMH_HEAVY_POINTS;   // expected points above which mode B runs
 
 // Division-free prefilter for the common case of large sets: decide from the
 // element's first stream word whether its FIRST point exceeds thr and the
