@@ -14,6 +14,9 @@
 
 namespace pmh {
 
+#ifndef PMH_REFRESH_EVERY
+#define PMH_REFRESH_EVERY 8   // batches between forced h_max refreshes
+#endif
 #ifndef PMH_HEAVY_POINTS
 #define PMH_HEAVY_POINTS 16.0   // measured best on config 2 (4 / 6 / 8 / 12 / 16 / 24 / 32 / 48 tried)
 #endif
@@ -122,7 +125,7 @@ __device__ __forceinline__ bool run_batch(SetCtx& c, const Tables& T, const uint
   }
   // refresh h_max after batches that lowered a slot (and every 8th)
   const bool changed = __any_sync(0xffffffffu, c.updates != upd0);
-  if (changed || ++c.since_refresh >= 8) {
+  if (changed || ++c.since_refresh >= PMH_REFRESH_EVERY) {
     hmax_refresh_warp(c, lane);
     c.since_refresh = 0;
   }

@@ -104,7 +104,10 @@ __device__ __forceinline__ void hmax_refresh_warp(SetCtx& c, int lane) {
 // Lazy Fisher-Yates (K:222-235).  Positions/values are 1-based; an absent
 // entry means perm[p] == p.
 // ---------------------------------------------------------------------------
-constexpr int SPARSE_FY_CAP = 12;
+#ifndef PMH_SPARSE_FY_CAP
+#define PMH_SPARSE_FY_CAP 16   // measured: 8 / 12 / 16 / 24 tried on config 2
+#endif
+constexpr int SPARSE_FY_CAP = PMH_SPARSE_FY_CAP;
 
 struct SparseFY {
   int32_t pos[SPARSE_FY_CAP];
