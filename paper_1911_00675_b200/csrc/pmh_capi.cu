@@ -26,6 +26,10 @@
 #include "pmh_harness.cuh"
 #include "pmh_ingest.h"
 
+#ifndef PMH_ORDER_COST_M
+#define PMH_ORDER_COST_M 7.0   // ProbMinHash set cost ~ n + c m (coupon phase) for the LPT order
+#endif
+
 using namespace pmh;
 
 namespace {
@@ -528,7 +532,7 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
                         split_cap > 0;
   OrderWs ow;
   // cost offset: ProbMinHash families pay ~m ln m points per set regardless of n
-  e = build_order(offsets, nsets, pmin ? 0 : (int64_t)(7.0 * (double)m), pmin ? -1 : small_n_for(m),
+  e = build_order(offsets, nsets, pmin ? 0 : (int64_t)(PMH_ORDER_COST_M * (double)m), pmin ? -1 : small_n_for(m),
                   pm_split ? split_n : 4096, st, &ow);
   if (e != cudaSuccess) return cuda_fail(e, "set ordering");
   int32_t* order = ow.order;
@@ -609,7 +613,7 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
         if (e2 != cudaSuccess) return e2;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SKETCH_THREADS, smem);
         if (per_sm < 1) per_sm = 1;
-        e2 = split_setup(offsets, order, nsets, (int64_t)(7.0 * (double)m), sp_n, sp_cap, m,
+        e2 = split_setup(offsets, order, nsets, (int64_t)(PMH_ORDER_COST_M * (double)m), sp_n, sp_cap, m,
                          stats_out, (long long)sms * per_sm, st, &sws);
         if (e2 != cudaSuccess) return e2;
         a.split_info = sws.sp.info;

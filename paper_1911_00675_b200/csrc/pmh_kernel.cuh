@@ -14,6 +14,9 @@
 
 namespace pmh {
 
+#ifndef PMH_CHUNK_DIV
+#define PMH_CHUNK_DIV 2       // element chunks per warp and set (at least)
+#endif
 #ifndef PMH_REFRESH_EVERY
 #define PMH_REFRESH_EVERY 8   // batches between forced h_max refreshes
 #endif
@@ -255,7 +258,7 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
   double tg = (double)m * (log((double)m) + a.tconst) / W;
   if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
   bool failed = false;
-  int64_t chunk = (n + 2 * nwarps - 1) / (2 * nwarps);
+  int64_t chunk = (n + PMH_CHUNK_DIV * nwarps - 1) / (PMH_CHUNK_DIV * nwarps);
   chunk = chunk < 1 ? 1 : (chunk > 32 * PMH_EPL ? 32 * PMH_EPL : chunk);
 
   for (int attempt = 0;; attempt++) {
