@@ -397,7 +397,7 @@ def main():
         torch.cuda.synchronize()
         # every step copies its inputs in and its signatures out (pinned host
         # memory) inside the timed region
-        e2e_s = timed_e2e(pipelined, max(args.e2e_steps, 6))
+        e2e_s = timed_e2e(pipelined, max(args.e2e_steps, 10))
         _lib.check(L.pmh_status_check(status.data_ptr(), ctypes.byref(err), sp), err.value)
     h2d = batch.ids.nbytes + batch.weights.nbytes + batch.offsets.nbytes
     d2h = len(variants) * S * M * 8
