@@ -20,6 +20,15 @@
 
 namespace pmh {
 
+// Bounds checks of a debug build (-DPMH_DEBUG_BOUNDS): trap on a violated
+// index invariant so a test run fails loudly instead of corrupting memory.
+#ifdef PMH_DEBUG_BOUNDS
+#define PMH_ASSERT(c) do { if (!(c)) __trap(); } while (0)
+#else
+#define PMH_ASSERT(c) do { } while (0)
+#endif
+
+
 constexpr uint64_t GOLDEN = 0x9E3779B97F4A7C15ULL;  // K:20
 constexpr uint64_t MIX1 = 0xBF58476D1CE4E5B9ULL;    // K:21
 constexpr uint64_t MIX2 = 0x94D049BB133111EBULL;    // K:22

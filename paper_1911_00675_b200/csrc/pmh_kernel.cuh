@@ -177,6 +177,7 @@ __device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const 
         const bool surv = act[j] && !first_point_rejects<F>(T, id[j], wv[j], thr);
         rej += act[j] && !surv;
         const unsigned sm = __ballot_sync(0xffffffffu, surv);
+        PMH_ASSERT(qn + __popc(sm) <= 160);
         if (surv) wscr->sq[qn + __popc(sm & ((1u << lane) - 1u))] = (int32_t)(base + (uint32_t)lane + 32u * j);
         qn += __popc(sm);
       }

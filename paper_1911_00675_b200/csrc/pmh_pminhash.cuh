@@ -210,6 +210,7 @@ __device__ __forceinline__ void pm64_check(uint64_t id, double winv, uint32_t e,
   uint64_t b = lo >> sh;
   if (sh > 11) b |= stream_word(id, wi + 2) << (64 - sh);
   b &= (1ULL << 53) - 1ULL;
+  PMH_ASSERT(t * PM64_C + q < (int64_t)tpg * PM64_C && q >= 0 && q < PM64_C);
   Slot* sl = &table[pm64_slot(t, q, tpg)];
   const double cur = __longlong_as_double((long long)*(volatile unsigned long long*)&sl->h);
   double h;
@@ -378,8 +379,10 @@ __device__ __forceinline__ void pm64_range(const PMinArgs& a, int64_t off, int64
             if (cand) pm64_candidates<EXPO>(cand, id, w, (uint32_t)e, t, tpg, table);
           } else if (total) {
             int pos = qn + x - c;
-            for (uint64_t cb = cand; cb; cb &= cb - 1)
+            for (uint64_t cb = cand; cb; cb &= cb - 1) {
+              PMH_ASSERT(pos < PM64_CQ);
               cq[pos++] = make_uint2((uint32_t)e, ((uint32_t)t << 6) | (uint32_t)(__ffsll((long long)cb) - 1));
+            }
             qn += total;
             __syncwarp();
             while (qn >= 32) {

@@ -72,6 +72,7 @@ __device__ __noinline__ void hmax_recompute_serial(SetCtx& c) {
 
 __device__ __forceinline__ void ctx_offer(SetCtx& c, int64_t k0, double x,
                                           int64_t e) {
+  PMH_ASSERT(k0 >= 0 && k0 < c.m);
   unsigned long long prev = slot_offer(&c.slots[k0], x, (unsigned long long)(e + c.eoff));
   if (prev == ~0ULL) return;
   c.updates++;

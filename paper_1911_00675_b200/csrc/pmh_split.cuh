@@ -158,6 +158,7 @@ __device__ __forceinline__ bool split_next_part(const SplitArgs& a, long long* s
   const int64_t k = t - a.part_base[lo];
   p->e0 = p->n * k / parts;
   p->e1 = p->n * (k + 1) / parts;
+  PMH_ASSERT(lo < a.info[0] && lo < a.split_cap && k < parts && p->e1 <= p->n && p->e0 < p->e1);
   return true;
 }
 

@@ -47,14 +47,19 @@ struct EpochFY {
   uint32_t* a;
   uint32_t ep;
   __device__ __forceinline__ int32_t get(int32_t p) const {
+    PMH_ASSERT(p >= 0 && p < 65536);
     const uint32_t v = a[p];
     return (v >> 16) == ep ? (int32_t)(v & 0xffffu) : p;
   }
-  __device__ __forceinline__ void set(int32_t p, int32_t v) { a[p] = (ep << 16) | (uint32_t)v; }
+  __device__ __forceinline__ void set(int32_t p, int32_t v) {
+    PMH_ASSERT(p >= 0 && p < 65536 && v >= 0 && v < 65536);
+    a[p] = (ep << 16) | (uint32_t)v;
+  }
 };
 
 __device__ __forceinline__ uint64_t win_bits(const uint64_t* w, uint32_t rel, uint32_t k) {
   const uint32_t i = rel >> 6, sh = rel & 63;
+  PMH_ASSERT(i < 65 && !(sh && sh + k > 64 && i + 1 >= 65));
   uint64_t v = w[i] >> sh;
   if (sh && sh + k > 64) v |= w[i + 1] << (64 - sh);
   return k == 64 ? v : (v & ((1ULL << k) - 1ULL));
@@ -77,6 +82,7 @@ __device__ __forceinline__ void win_load(WarpScratch& ws, uint64_t id, uint64_t 
 
 // offer with a refresh trigger instead of an inline serial recompute
 __device__ __forceinline__ bool offer_trig(SetCtx& c, int64_t k0, double x, int64_t e) {
+  PMH_ASSERT(k0 >= 0 && k0 < c.m);
   unsigned long long prev = slot_offer(&c.slots[k0], x, (unsigned long long)(e + c.eoff));
   if (prev == ~0ULL) return false;
   c.updates++;
