@@ -110,3 +110,34 @@ def test_probminhash_split_sets_vs_oracle(monkeypatch, cap, algo):
         ref, _ = orc.sketch_csr(algo, m, batch.ids, w, batch.offsets, threads=8)
         got, _ = _gpu_sig(algo, m, batch)
         assert (got != ref).sum() == 0, (algo, m)
+
+
+def _edge_batch():
+    from paper_1911_00675_b200.datagen import CSRBatch
+    sets = [
+        ([0, 2**64 - 1, 1, 2**63], [1.0, 1.0, 1.0, 1.0]),                # boundary ids
+        ([5, 6, 7], [1e-300, 1.0, 1e300]),                                   # extreme weights
+        ([11, 12], [5e-324, 2.0]),                                           # denormal weight
+        ([21, 21, 22], [1.0, 3.0, 0.5]),                                     # duplicate id (validate=False)
+        ([31], [123.456]),
+        (list(range(100, 140)), list(np.geomspace(1e-12, 1e12, 40))),      # 24 decades
+    ]
+    ids = np.concatenate([np.array(i, np.uint64) for i, _ in sets])
+    w = np.concatenate([np.array(x, np.float64) for _, x in sets])
+    off = np.concatenate([[0], np.cumsum([len(i) for i, _ in sets])]).astype(np.int64)
+    return CSRBatch(ids, w, off, "edge")
+
+
+@pytest.mark.parametrize("algo", ["pminhash", "probminhash1", "probminhash1a", "probminhash2",
+                                  "probminhash3", "probminhash3a", "probminhash4"])
+@pytest.mark.parametrize("m", [1, 2, 63, 64, 1000, 4096])
+def test_edge_inputs_vs_oracle(algo, m):
+    """Boundary ids, extreme / denormal weights, duplicate ids and boundary m
+    (1, 2, non-multiples of 64, 4096) give the oracle's signatures."""
+    from oracle import oracle as orc
+    if m < 2 and algo in ("probminhash3", "probminhash3a", "probminhash4"):
+        pytest.skip("m >= 2 required")
+    batch = _edge_batch()
+    ref, _ = orc.sketch_csr(algo, m, batch.ids, batch.weights, batch.offsets)
+    got, _ = _gpu_sig(algo, m, batch)
+    assert (got != ref).sum() == 0
