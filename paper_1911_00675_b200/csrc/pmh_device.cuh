@@ -54,6 +54,13 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // K:40-44
   return z ^ (z >> 31);
 }
 
+// mix64 without its final xorshift (out = z ^ (z >> 31)); bits 33..63 of z
+// and of mix64's output agree (the P-MinHash body tests those on z directly)
+__device__ __forceinline__ uint64_t mix64_z(uint64_t x) {
+  uint64_t z = (x ^ (x >> 30)) * MIX1;
+  return (z ^ (z >> 27)) * MIX2;
+}
+
 
 // word j (1-based) of the stream seeded with `seed`
 __device__ __forceinline__ uint64_t stream_word(uint64_t seed, uint64_t j) {

@@ -354,9 +354,11 @@ __device__ __forceinline__ void pm64_range(const PMinArgs& a, int64_t off, int64
         uint64_t st = id + wbase * GOLDEN;
         const uint32_t one = *(volatile uint32_t*)&s_one;
         uint32_t c_lo = 0, c_hi = 0;
-#define MIX mix64
+#define MIXZ mix64_z
+#define PM64_TEST(x, thr, mask, bit) if ((x) <= (thr)) mask |= (bit)
 #include "pm64_body.inc"
-#undef MIX
+#undef PM64_TEST
+#undef MIXZ
         const uint64_t cand = live ? (((uint64_t)c_hi << 32) | c_lo) : 0ULL;
         // candidates are cheap (1-2 stream words + a compare against the
         // slot's own minimum) but scattered: a few lanes per warp-step.  They
