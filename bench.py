@@ -42,9 +42,14 @@ VARIANTS = ["pminhash", "probminhash1", "probminhash1a", "probminhash2",
             "probminhash3", "probminhash3a", "probminhash4"]
 METRIC = "set elements hashed/sec at m=1024"
 E2E_DEPTH = 2   # pipelined e2e: batches in flight
-# splitmix64 word: 64-bit add (2) + 3 x (64-bit shift + xor: 4) = 14 ALU ops;
-# a 53-bit draw uses 53/64 word, + 2 ops (extract 32 bits, compare)
-ALU_OPS_PER_DRAW = 14.0 * 53.0 / 64.0 + 2.0
+# ALU-pipe work of the P-MinHash schedule (tools/gen_pm64.py) per 64 draws =
+# 53 splitmix64 words: per word the low half of the counter add (1; the high
+# half runs on the FMA pipe) and two 64-bit xor-shifts (4 each); the final
+# xor-shift's low half (2) on the 44 words holding a draw's top bits below
+# bit 44, its high half (2) on 12 of them; 23 funnel extractions; one compare
+# per draw.  (The full splitmix64 + exact extraction would be 13.6 per draw.)
+ALU_OPS_PER_DRAW = (53 * 9 + 44 * 2 + 12 * 2 + 23) / 64.0 + 1.0
+ALU_OPS_PER_DRAW_FULL_MIX = 14.0 * 53.0 / 64.0 + 2.0
 # dram read+write bytes per launch from `ncu --set full` of the full config-2
 # launch (profiles/r01_ncu_pminhash64_full_config2.txt); the read side exceeds
 # the algorithmic 1.39 GB of ids/weights by the weight-sum pre-pass of the
@@ -418,10 +423,8 @@ def main():
     _lib.check(L.pmh_probe_alu_peak(ctypes.byref(gops), ctypes.byref(pms)))
     if dom == "pminhash":
         # ncu: the P-MinHash kernel is bound by the 32-bit ALU pipe.  Algorithmic
-        # ALU work = N*m draws x ALU_OPS_PER_DRAW (splitmix64: 64-bit add + three
-        # 64-bit xor-shifts = 14 ALU ops per word, 53/64 word per 53-bit draw,
-        # + 2 ops to extract and compare the draw; the two 64-bit multiplies run
-        # on the FMA pipe) -- see DESIGN.md §4.
+        # ALU work = N*m draws x ALU_OPS_PER_DRAW (the schedule's required ALU
+        # ops; the two 64-bit multiplies run on the FMA pipe) -- DESIGN.md §4.
         alu_ops = float(N) * M * ALU_OPS_PER_DRAW
         achieved = alu_ops / (per_variant_ms[dom] / 1e3) / 1e9
         roofline = {
@@ -429,10 +432,11 @@ def main():
             "peak": gops.value, "unit": "Gop/s (32-bit ALU pipe)",
             "frac": achieved / gops.value, "traffic": TRAFFIC_BYTES.get(dom),
             "peak_source": "measured live: pmh_probe_alu_peak (LOP3 chains, full occupancy)",
-            "note": ("integer-ALU-bound (splitmix64 per draw; ncu: ALU pipe ~83%, DRAM ~0.4%, "
+            "note": ("integer-ALU- and issue-bound (splitmix64 per draw; ncu: ALU pipe ~81%, FMA-heavy ~62%, issue ~76%, DRAM ~0.4%, "
                      "no GEMM-shaped work), so neither the HBM nor the tensor roofline applies; "
                      "the HBM figures are given below for reference"),
             "algorithmic_ops": alu_ops, "ops_per_draw": ALU_OPS_PER_DRAW,
+            "ops_per_draw_full_mix64": ALU_OPS_PER_DRAW_FULL_MIX,
             "hbm": {"achieved_GBps": hbm_achieved, "peak_GBps": hbm_peak,
                     "frac": hbm_achieved / hbm_peak, "peak_source": peak_src,
                     "algorithmic_bytes": alg_bytes},

@@ -147,3 +147,23 @@ def test_bbit_host_helpers():
     for c in (0, 10, 25, 50):
         p = 2.0 ** -b
         assert bbit_estimate(c, m, b) == min(1.0, max(0.0, (c / m - p) / (1 - p)))
+
+
+def test_nonstreaming_api_validation():
+    """Non-streaming PMH2/PMH4 (configs[3]): argument checks run on the host
+    before any CUDA call, with the reference's exception types."""
+    import math
+    from paper_1911_00675_b200 import (EmptyInputError, InvalidParamsError,
+                                       NONSTREAMING_ALGORITHMS, WeightedSet,
+                                       probminhash2_nonstreaming, probminhash4_nonstreaming)
+    assert set(NONSTREAMING_ALGORITHMS) == {"nonstreaming2", "nonstreaming4"}
+    ws = WeightedSet([(1, 1.0), (2, 0.5)])
+    for bad in (0.0, -1.0, math.inf, math.nan):
+        with pytest.raises(InvalidParamsError):
+            probminhash2_nonstreaming(ws, 16, total_weight=bad)
+        with pytest.raises(InvalidParamsError):
+            probminhash4_nonstreaming(ws, 16, total_weight=bad)
+    with pytest.raises(InvalidParamsError):
+        probminhash4_nonstreaming(ws, 1)           # m >= 2 like probminhash4
+    with pytest.raises(EmptyInputError):
+        probminhash2_nonstreaming(WeightedSet([]), 16)

@@ -279,6 +279,26 @@ def test_config4_pareto_m64_subset():
         assert (sigs_to_numpy(sig) != ref).sum() == 0, algo
 
 
+@pytest.mark.parametrize("m", [2, 64, 1024])
+def test_nonstreaming_single_set_api(m):
+    """probminhash2/4_nonstreaming == streaming signatures == oracle, with and
+    without a total weight (also a wrong one: it is scheduling-only)."""
+    from paper_1911_00675_b200 import (WeightedSet, probminhash2_nonstreaming,
+                                       probminhash4_nonstreaming)
+    b = datagen.config4(nsets=12, seed=3)
+    for i in range(b.nsets):
+        lo, hi = b.offsets[i], b.offsets[i + 1]
+        ws = WeightedSet.from_arrays(b.ids[lo:hi], b.weights[lo:hi])
+        W = float(b.weights[lo:hi].sum())
+        for algo, fn in (("probminhash2", probminhash2_nonstreaming),
+                         ("probminhash4", probminhash4_nonstreaming)):
+            ref, _ = orc.sketch_csr(algo, m, b.ids[lo:hi], b.weights[lo:hi],
+                                    np.array([0, hi - lo], np.int64))
+            for tw in (None, W, 1e-3 * W):
+                sig, _ = fn(ws, m, total_weight=tw)
+                assert np.array_equal(sig.components, ref[0]), (algo, i, tw)
+
+
 def test_empty_set_in_batch_reports_index():
     ids = np.arange(10, dtype=np.uint64)
     off = np.array([0, 4, 4, 10], np.int64)
