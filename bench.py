@@ -54,7 +54,7 @@ ALU_OPS_PER_DRAW_FULL_MIX = 14.0 * 53.0 / 64.0 + 2.0
 # launch (profiles/r01_ncu_pminhash64_full_config2.txt); the read side exceeds
 # the algorithmic 1.39 GB of ids/weights by the weight-sum pre-pass of the
 # threshold guess (~0.7 GB, a second read of the weights)
-TRAFFIC_BYTES = {"pminhash": 2182183000 + 52388864}
+TRAFFIC_BYTES = {"pminhash": 2177812000 + 55420672}
 UNIT = "elements/s"
 
 
