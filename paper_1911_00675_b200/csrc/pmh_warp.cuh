@@ -278,6 +278,40 @@ __device__ __forceinline__ uint32_t accept_mask(const uint64_t* w, uint32_t pos,
   return acc;
 }
 
+// accept_mask for a compile-time label width and round range: the field
+// shifts, masks and bit positions become immediates and the compares 32-bit
+// (fields and R < 2^KB <= 2^32).  Rounds [T0, T1) start at window loads
+// aligned to T0, so the fields of one load are u = 0 .. FPW-1.
+template <uint32_t KB, uint32_t T0, uint32_t T1>
+__device__ __forceinline__ uint32_t accept_mask_k(const uint64_t* w, uint32_t pos, uint32_t R) {
+  constexpr uint32_t FPW = 64u / KB;
+  constexpr uint64_t MASK = (1ULL << KB) - 1ULL;
+  uint32_t acc = 0;
+#pragma unroll
+  for (uint32_t t = T0; t < T1; t += FPW) {
+    const uint32_t p = pos + KB * t, i = p >> 6, sh = p & 63;
+    const uint64_t win = sh ? (w[i] >> sh) | (w[i + 1] << (64 - sh)) : w[i];
+#pragma unroll
+    for (uint32_t u = 0; u < FPW; u++)
+      if (t + u < T1) acc |= ((uint32_t)((win >> (KB * u)) & MASK) < R ? 1u : 0u) << (t + u);
+  }
+  return acc;
+}
+
+// the label widths of the configured m (64, 256, 1024, 4096: kb = 6, 8, 10,
+// 12 for the first half of the ranges) specialised, the rest generic
+template <uint32_t T0, uint32_t T1>
+__device__ __forceinline__ uint32_t accept_mask_sel(const uint64_t* w, uint32_t pos, uint32_t kb,
+                                                    uint64_t R, uint32_t fpw) {
+  switch (kb) {
+    case 6: return accept_mask_k<6, T0, T1>(w, pos, (uint32_t)R);
+    case 8: return accept_mask_k<8, T0, T1>(w, pos, (uint32_t)R);
+    case 10: return accept_mask_k<10, T0, T1>(w, pos, (uint32_t)R);
+    case 12: return accept_mask_k<12, T0, T1>(w, pos, (uint32_t)R);
+    default: return accept_mask(w, pos, kb, R, T0, T1, fpw);
+  }
+}
+
 // Warp-parallel version of parse_fy_cursor.  For a run of points whose
 // Fisher-Yates range R = m - pt + 1 shares the label width kb, point k starts
 // at base_k + kb * Y_k, where base_k = rel0 + k (53 + kb) and Y_k is the number
@@ -315,7 +349,7 @@ __device__ void parse_fy_parallel(const SetCtx& c, WarpScratch& ws, uint64_t id,
   // rounds are only decoded when the scan runs past them
   const uint32_t fpw = 64u / kb;   // label fields per 64-bit window load
   const bool mine = (uint32_t)lane < qmax;
-  uint32_t acc = mine ? accept_mask(ws.words, base + 53u, kb, (uint64_t)R, 0u, ACC_ROUNDS0, fpw)
+  uint32_t acc = mine ? accept_mask_sel<0u, ACC_ROUNDS0>(ws.words, base + 53u, kb, (uint64_t)R, fpw)
                       : 0u;
   bool full = false;
   // Y_{k+1} = first accepted round >= Y_k of point k.  Y only moves at points
@@ -330,7 +364,7 @@ __device__ void parse_fy_parallel(const SetCtx& c, WarpScratch& ws, uint64_t id,
     if (j >= qmax) break;
     const uint32_t am = __shfl_sync(0xffffffffu, acc, (int)j) >> Y;
     if (am == 0 && !full) {  // decode the remaining rounds and retry this point
-      if (mine) acc |= accept_mask(ws.words, base + 53u, kb, (uint64_t)R, ACC_ROUNDS0, 24u, fpw);
+      if (mine) acc |= accept_mask_sel<ACC_ROUNDS0, 24u>(ws.words, base + 53u, kb, (uint64_t)R, fpw);
       full = true;
       continue;
     }
