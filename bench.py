@@ -226,6 +226,10 @@ def main():
                     help="run the step's variants concurrently (pmh_sketch_csr_multi_async); "
                          "per-variant times then come from separate untimed passes")
     ap.add_argument("--variants", default=",".join(VARIANTS))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak (default): every rank sketches its own config-2 batch; strong: "
+                         "ONE config-2 batch sharded across the ranks by estimated cost "
+                         "(dist.shard_ranges_multi, no collective on the data path)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -246,7 +250,13 @@ def main():
 
     variants = args.variants.split(",")
     L = _lib.load()
-    batch = datagen.config2(seed=2 + rank)
+    if args.scaling == "strong":
+        from paper_1911_00675_b200.dist import local_batch, shard_ranges_multi
+        batch = datagen.config2(seed=2)
+        if world > 1:
+            batch = local_batch(batch, shard_ranges_multi(batch.offsets, world, M, variants)[rank])
+    else:
+        batch = datagen.config2(seed=2 + rank)
     N, S = batch.nelems, batch.nsets
     ids = to_device_u64(batch.ids)
     w = to_device_f64(batch.weights)
@@ -330,7 +340,8 @@ def main():
     ms_step = ms_total / args.steps
     per_variant_ms = {v: float(np.mean([a.elapsed_time(b) for a, b in ev[v]])) if ev[v] else None
                       for v in variants}
-    # whole-job elements: every rank sketches its own batch (seed 2 + rank)
+    # whole-job elements: weak -- every rank sketches its own batch (seed 2 +
+    # rank); strong -- the ranks' shards of one batch (the sum is that batch)
     n_total = N
     if world > 1:
         t = torch.tensor([float(N)], device="cuda", dtype=torch.float64)
@@ -455,7 +466,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f64+u64", "data": "synthetic",
         "config": {"workload": "config2: 10k log-uniform weighted sets, 7 weighted variants, m=1024",
                    "sets_per_gpu": S, "elements_per_gpu": N, "m": M,

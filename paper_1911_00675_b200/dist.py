@@ -35,7 +35,17 @@ def set_costs(offsets, m: int, algo: str) -> np.ndarray:
 def shard_ranges(offsets, world: int, m: int = 1024, algo: str = "probminhash3"):
     """Contiguous set ranges [(s0, s1)] per rank with near-equal total cost
     (greedy split of the cumulative cost curve)."""
-    costs = set_costs(offsets, m, algo)
+    return _split_cost(set_costs(offsets, m, algo), world)
+
+
+def shard_ranges_multi(offsets, world: int, m: int, algos):
+    """shard_ranges for a step that runs several algorithms over the same
+    batch: the cost of a set is the sum of its per-algorithm costs."""
+    costs = sum(set_costs(offsets, m, a) for a in algos)
+    return _split_cost(costs, world)
+
+
+def _split_cost(costs, world: int):
     S = costs.size
     if world <= 1 or S == 0:
         return [(0, S)]
@@ -43,10 +53,8 @@ def shard_ranges(offsets, world: int, m: int = 1024, algo: str = "probminhash3")
     total = cum[-1]
     bounds = [0]
     for r in range(1, world):
-        target = total * r / world
-        b = int(np.searchsorted(cum, target, side="left"))
-        b = min(max(b, bounds[-1]), S)
-        bounds.append(b)
+        b = int(np.searchsorted(cum, total * r / world, side="left"))
+        bounds.append(min(max(b, bounds[-1]), S))
     bounds.append(S)
     return [(bounds[r], bounds[r + 1]) for r in range(world)]
 

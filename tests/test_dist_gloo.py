@@ -63,6 +63,24 @@ def test_shard_ranges_balanced_and_complete():
         assert max(loads) <= 1.15 * c.sum() / world + c.max()
 
 
+def test_shard_ranges_multi_strong_scaling_split():
+    """bench.py --scaling strong: one config-2 batch split for the 7-variant
+    step; shards tile the batch and balance the summed per-variant cost."""
+    b = datagen.config2(nsets=3000)
+    algos = ["pminhash", "probminhash1", "probminhash1a", "probminhash2", "probminhash3",
+             "probminhash3a", "probminhash4"]
+    c = sum(pdist.set_costs(b.offsets, 1024, a) for a in algos)
+    for world in (1, 2, 4, 8):
+        rngs = pdist.shard_ranges_multi(b.offsets, world, 1024, algos)
+        assert rngs[0][0] == 0 and rngs[-1][1] == b.nsets
+        assert all(rngs[i][1] == rngs[i + 1][0] for i in range(world - 1))
+        loads = [c[a:z].sum() for a, z in rngs]
+        assert max(loads) <= c.sum() / world + c.max()
+        parts = [pdist.local_batch(b, r) for r in rngs]
+        assert sum(p.nelems for p in parts) == b.nelems
+        assert np.array_equal(np.concatenate([p.ids for p in parts]), b.ids)
+
+
 def test_block_rows_cover_triangle_balanced():
     for n, tile, world in ((1000, 64, 3), (100000, 4096, 8), (10, 3, 2)):
         rows = pdist.block_rows(n, tile, world)
