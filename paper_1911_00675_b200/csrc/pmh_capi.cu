@@ -141,10 +141,24 @@ int64_t min_m(int algo) {
 }
 
 template <int F>
-cudaError_t launch_family(const SketchArgs& a, cudaStream_t st) {
+cudaError_t launch_family(const SketchArgs& a0, cudaStream_t st) {
+  const int64_t grid0 = a0.nsets < 2147483647LL ? a0.nsets : 2147483647LL;
+  if constexpr (family_uses_fy(F)) {
+    if (sketch_use_big(F, a0.m)) {  // large m: 16 warps per set on 16-bit Fisher-Yates maps
+      SketchArgs a = a0;
+      a.fy16 = 1;
+      const size_t smem = sketch_smem_bytes(F, a.m, SKETCH_THREADS_BIG, true);
+      cudaError_t e = cudaFuncSetAttribute(sketch_sets_kernel<F, SKETCH_THREADS_BIG>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      sketch_sets_kernel<F, SKETCH_THREADS_BIG><<<(unsigned)grid0, SKETCH_THREADS_BIG, smem, st>>>(a);
+      return cudaGetLastError();
+    }
+  }
+  const SketchArgs& a = a0;
   const int threads = SKETCH_THREADS;
-  const size_t smem = sketch_smem_bytes(F, a.m, threads);
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  const size_t smem = sketch_smem_bytes(F, a.m, threads, a.fy16 != 0);
+  if (smem > SMEM_DYN_MAX) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(sketch_sets_kernel<F>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -372,7 +386,7 @@ cudaError_t launch_small(const SketchArgs& a, cudaStream_t st) {
   int wpc = (int)((96 * 1024) / per_warp);
   wpc = wpc < 1 ? 1 : (wpc > 4 ? 4 : wpc);
   const size_t smem = per_warp * (size_t)wpc;
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  if (smem > SMEM_DYN_MAX) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(sketch_small_kernel<F>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -392,7 +406,8 @@ int validate_sketch(int algo, int64_t m, const double* weights, int64_t nsets) {
     return set_error(PMH_ERR_INVALID, "unsupported algorithm id " + std::to_string(algo));
   if (m < min_m(algo))
     return set_error(PMH_ERR_INVALID, "signature size must be >= " + std::to_string(min_m(algo)));
-  if (fam != 0 && sketch_smem_bytes(fam, m, SKETCH_THREADS) > 227 * 1024)
+  if (fam != 0 && (sketch_smem_bytes(fam, m, SKETCH_THREADS, sketch_fy16_256(fam, m)) > SMEM_DYN_MAX ||
+                   (sketch_fy16_256(fam, m) && m >= 8192)))
     return set_error(PMH_ERR_INVALID, "signature size too large for the shared-memory slot table");
   if ((algo == ALG_PMINHASH || algo == ALG_MINHASH) && m > 64LL * PMIN_THREADS)
     return set_error(PMH_ERR_INVALID, "signature size too large for the P-MinHash kernel");
@@ -511,7 +526,7 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
         threads /= 2;
         smem = sizeof(Slot) * (size_t)m + sizeof(int32_t) * (size_t)m * (threads / 32);
       }
-      if (smem > 227 * 1024) return set_error(PMH_ERR_INVALID, "signature size too large");
+      if (smem > SMEM_DYN_MAX) return set_error(PMH_ERR_INVALID, "signature size too large");
       PMH_CUDA(cudaFuncSetAttribute(superminhash_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       superminhash_kernel<<<(unsigned)grid, threads, smem, st>>>(b);
@@ -563,6 +578,7 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
     a.err_flags = flags;
     a.err_set = d_err_set;
     a.T = *tp;
+    a.fy16 = sketch_fy16_256(fam, m) ? 1 : 0;
     // threshold guess m (ln m + c) / W: c = 3 measured best on config 2
     // (2 - 6 % faster PMH2/PMH4 than c = 4; ~5% of sets retry with 4 tg)
     a.tconst = 3.0;
@@ -603,7 +619,7 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
     if (const char* ev = getenv("PMH_SPLIT_CAP")) sp_cap = atoll(ev);
     if (sp_cap > (1LL << 24) / m) sp_cap = (1LL << 24) / m;
     auto split = [&]() -> cudaError_t {
-      const size_t smem = sketch_smem_bytes(fam, m, SKETCH_THREADS);
+      const size_t smem = sketch_smem_bytes(fam, m, SKETCH_THREADS, a.fy16 != 0);
       int dev = 0, sms = 148, per_sm = 1;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -52,13 +52,38 @@ __device__ __forceinline__ bool first_point_rejects(const Tables& T, uint64_t id
   }
 }
 constexpr int SKETCH_THREADS = 256;
+// dynamic shared memory per CTA: the 227 KB opt-in limit counts the kernels'
+// static __shared__ state too (SetShared and friends, < 1 KB)
+constexpr size_t SMEM_DYN_MAX = 227 * 1024 - 1024;
 
-__host__ __device__ inline size_t sketch_smem_bytes(int family, int64_t m, int threads) {
+// bytes of one warp's dense Fisher-Yates map (16-byte multiple)
+__host__ __device__ inline size_t fy_map_bytes(int64_t m, bool fy16) {
+  return ((fy16 ? 2 : 4) * (size_t)(m + 1) + 15) & ~(size_t)15;
+}
+
+__host__ __device__ inline size_t sketch_smem_bytes(int family, int64_t m, int threads,
+                                                    bool fy16 = false) {
   const int nw = threads / 32;
   size_t b = sizeof(Slot) * (size_t)m;
   b += sizeof(WarpScratch) * (size_t)nw;
-  if (family_uses_fy(family)) b += sizeof(uint32_t) * (size_t)(m + 1) * (size_t)nw;
+  if (family_uses_fy(family)) b += fy_map_bytes(m, fy16) * (size_t)nw;
   return (b + 15) & ~(size_t)15;
+}
+
+// 256-thread CTAs keep 32-bit Fisher-Yates maps while they fit; beyond that
+// (m > 4516) the maps are 16-bit (m < 8192 required by the 13-bit values),
+// which extends the Fisher-Yates families from m = 4516 to m = 6775.
+__host__ __device__ inline bool sketch_fy16_256(int family, int64_t m) {
+  return family_uses_fy(family) && sketch_smem_bytes(family, m, SKETCH_THREADS, false) > SMEM_DYN_MAX;
+}
+
+// Large m: the slot table alone is 16 m bytes, so the CTA kernel runs ONE set
+// per SM; the Fisher-Yates families then run 16 warps per CTA on 16-bit maps
+// (2x the warps of the 256-thread layout in the same shared memory).
+constexpr int SKETCH_THREADS_BIG = 512;
+__host__ __device__ inline bool sketch_use_big(int family, int64_t m) {
+  return family_uses_fy(family) && m > 2048 && m < 8192 &&
+         sketch_smem_bytes(family, m, SKETCH_THREADS_BIG, true) <= SMEM_DYN_MAX;
 }
 
 // Per-warp element loop shared by the CTA-per-set and warp-per-set kernels:
@@ -256,6 +281,7 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
   c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
   c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
   c.eoff = e0;
+  c.fy16 = a.fy16 != 0;
   double tg = (double)m * (log((double)m) + a.tconst) / W;
   if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
   bool failed = false;
@@ -304,28 +330,30 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
 
 template <int F>
 __device__ __forceinline__ void sketch_cta_setup(unsigned char* smem, int64_t m, Slot** slots,
-                                                 WarpScratch** wscr, uint32_t** fy_dense) {
+                                                 WarpScratch** wscr, uint32_t** fy_dense,
+                                                 bool fy16) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   *slots = reinterpret_cast<Slot*>(smem);
   *wscr = reinterpret_cast<WarpScratch*>(smem + sizeof(Slot) * m) + wid;
-  *fy_dense = reinterpret_cast<uint32_t*>(smem + sizeof(Slot) * m + sizeof(WarpScratch) * nwarps) +
-              (size_t)wid * (m + 1);
+  *fy_dense = reinterpret_cast<uint32_t*>(smem + sizeof(Slot) * m + sizeof(WarpScratch) * nwarps +
+                                          fy_map_bytes(m, fy16) * (size_t)wid);
   if (family_uses_fy(F)) {  // epoch 0 never matches: the map starts empty
-    for (int64_t p = lane; p <= m; p += 32) (*fy_dense)[p] = 0;
+    fy_clear(*fy_dense, m, fy16, lane);
     if (lane == 0) (*wscr)->epoch = 0;
   }
 }
 
-template <int F>
-__global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS) sketch_sets_kernel(SketchArgs a) {
+template <int F, int NT = SKETCH_THREADS>
+__global__ void __launch_bounds__(NT, (NT == SKETCH_THREADS ? SKETCH_MINBLOCKS : 1))
+    sketch_sets_kernel(SketchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SetShared sh;
   const int64_t m = a.m;
   Slot* slots;
   WarpScratch* wscr;
   uint32_t* fy_dense;
-  sketch_cta_setup<F>(smem, m, &slots, &wscr, &fy_dense);
+  sketch_cta_setup<F>(smem, m, &slots, &wscr, &fy_dense, a.fy16 != 0);
   // mode B needs static point offsets (power-of-two m) unless the family
   // parses its bit offsets (Fisher-Yates families)
   const bool warp_ok = family_uses_fy(F) || ((m & (m - 1)) == 0);
@@ -377,7 +405,7 @@ __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS)
   Slot* slots;
   WarpScratch* wscr;
   uint32_t* fy_dense;
-  sketch_cta_setup<F>(smem, m, &slots, &wscr, &fy_dense);
+  sketch_cta_setup<F>(smem, m, &slots, &wscr, &fy_dense, a.fy16 != 0);
   const bool warp_ok = family_uses_fy(F) || ((m & (m - 1)) == 0);
   SplitPart p;
   while (split_next_part(sp, &s_t, &p)) {
@@ -488,6 +516,7 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
     c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
     c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
     c.eoff = 0;
+    c.fy16 = false;
     double tg = (double)m * (log((double)m) + a.tconst) / W;
     if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
     bool failed = false;

@@ -42,20 +42,39 @@ struct WarpScratch {
 
 // Dense per-warp Fisher-Yates map with O(1) reset: entry = epoch << 16 | value
 // (the versioned lazy permutation of K:222-235 / lazyperm.py, one epoch per
-// element).  Requires m < 65536.
+// element).  Requires m < 65536.  With h16 the entries are 16-bit, epoch << 13
+// | value (m < 8192, epochs 1..7, the map cleared when they wrap): half the
+// shared memory, so large-m sets run 16 warps per CTA (FY_EPOCHS16).
+constexpr uint32_t FY_EPOCHS32 = 0x10000u, FY_EPOCHS16 = 8u;
 struct EpochFY {
   uint32_t* a;
   uint32_t ep;
+  bool h16;
   __device__ __forceinline__ int32_t get(int32_t p) const {
-    PMH_ASSERT(p >= 0 && p < 65536);
+    PMH_ASSERT(p >= 0 && p < (h16 ? 8192 : 65536));
+    if (h16) {
+      const uint32_t v = reinterpret_cast<const uint16_t*>(a)[p];
+      return (v >> 13) == ep ? (int32_t)(v & 0x1fffu) : p;
+    }
     const uint32_t v = a[p];
     return (v >> 16) == ep ? (int32_t)(v & 0xffffu) : p;
   }
   __device__ __forceinline__ void set(int32_t p, int32_t v) {
-    PMH_ASSERT(p >= 0 && p < 65536 && v >= 0 && v < 65536);
-    a[p] = (ep << 16) | (uint32_t)v;
+    PMH_ASSERT(p >= 0 && v >= 0 && (h16 ? (p < 8192 && v < 8192 && ep < 8) : (p < 65536 && v < 65536)));
+    if (h16) reinterpret_cast<uint16_t*>(a)[p] = (uint16_t)((ep << 13) | (uint32_t)v);
+    else a[p] = (ep << 16) | (uint32_t)v;
   }
 };
+
+// clear a dense map (entries 0..m) -- epoch 0 never matches
+__device__ __forceinline__ void fy_clear(uint32_t* fy, int64_t m, bool h16, int lane) {
+  if (h16) {
+    uint16_t* f = reinterpret_cast<uint16_t*>(fy);
+    for (int64_t p = lane; p <= m; p += 32) f[p] = 0;
+  } else {
+    for (int64_t p = lane; p <= m; p += 32) fy[p] = 0;
+  }
+}
 
 __device__ __forceinline__ uint64_t win_bits(const uint64_t* w, uint32_t rel, uint32_t k) {
   const uint32_t i = rel >> 6, sh = rel & 63;
@@ -439,13 +458,13 @@ __device__ int warp_el_fy(SetCtx& c, const Tables& T, WarpScratch& ws, uint32_t*
                           int64_t e, uint64_t id, double winv) {
   const int64_t m = c.m;
   uint32_t ep = ws.epoch + 1;
-  if (ep >= 0x10000u) {  // epoch wrap: clear the map once every 65535 elements
-    for (int64_t p = lane; p <= m; p += 32) fy[p] = 0;
+  if (ep >= (c.fy16 ? FY_EPOCHS16 : FY_EPOCHS32)) {  // epoch wrap: clear the map
+    fy_clear(fy, m, c.fy16, lane);
     ep = 1;
   }
   __syncwarp();
   if (lane == 0) ws.epoch = ep;
-  EpochFY efy{fy, ep};
+  EpochFY efy{fy, ep, c.fy16};
   uint64_t off = 0;
   int64_t i = 1;
   double x = 0.0;

@@ -141,3 +141,38 @@ def test_edge_inputs_vs_oracle(algo, m):
     ref, _ = orc.sketch_csr(algo, m, batch.ids, batch.weights, batch.offsets)
     got, _ = _gpu_sig(algo, m, batch)
     assert (got != ref).sum() == 0
+
+
+@pytest.mark.parametrize("algo", ["probminhash2", "probminhash4", "unweighted2", "unweighted4"])
+@pytest.mark.parametrize("m", [2049, 3000, 4096, 4200, 5000, 6775])
+def test_large_m_fisher_yates_16bit_maps_vs_oracle(algo, m):
+    """Large m on 16-bit epoch maps (7 epochs, cleared on wrap: many wraps per
+    set here): 2048 < m <= 4212 run 512-thread CTAs (sketch_use_big; 2049 and
+    3000 are not powers of two), 4516 < m <= 6775 keep 256 threads with 16-bit
+    maps (sketch_fy16_256; 6775 is the largest m that fits)."""
+    from oracle import oracle as orc
+    from paper_1911_00675_b200 import datagen
+    rng = np.random.default_rng(m)
+    sizes = np.concatenate([[1, 2, 5, 17, 40], rng.integers(50, 400, 5)])
+    batch = datagen.random_sets(int(rng.integers(1 << 30)), sizes, "pareto1.5")
+    if algo.startswith("unweighted"):
+        batch = type(batch)(batch.ids, None, batch.offsets, batch.name)
+    ref, _ = orc.sketch_csr(algo, m, batch.ids, batch.weights, batch.offsets, threads=8)
+    got, _ = _gpu_sig(algo, m, batch)
+    assert (got != ref).sum() == 0
+
+
+def test_large_m_limits():
+    """Beyond the shared-memory slot table the C ABI refuses the call before
+    any launch (InvalidParamsError), family by family."""
+    from paper_1911_00675_b200 import InvalidParamsError
+    from paper_1911_00675_b200 import datagen
+    batch = datagen.random_sets(5, [3, 30], "exp")
+    with pytest.raises(InvalidParamsError):
+        _gpu_sig("probminhash2", 6776, batch)
+    with pytest.raises(InvalidParamsError):
+        _gpu_sig("probminhash1", 13553, batch)
+    got, _ = _gpu_sig("probminhash1", 6776, batch)      # no Fisher-Yates map: fits
+    from oracle import oracle as orc
+    ref, _ = orc.sketch_csr("probminhash1", 6776, batch.ids, batch.weights, batch.offsets)
+    assert (got != ref).sum() == 0
