@@ -144,20 +144,25 @@ template <int F>
 cudaError_t launch_family(const SketchArgs& a0, cudaStream_t st) {
   const int64_t grid0 = a0.nsets < 2147483647LL ? a0.nsets : 2147483647LL;
   if constexpr (family_uses_fy(F)) {
-    if (sketch_use_big(F, a0.m)) {  // large m: 16 warps per set on 16-bit Fisher-Yates maps
-      SketchArgs a = a0;
-      a.fy16 = 1;
-      const size_t smem = sketch_smem_bytes(F, a.m, SKETCH_THREADS_BIG, true);
-      cudaError_t e = cudaFuncSetAttribute(sketch_sets_kernel<F, SKETCH_THREADS_BIG>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // large m: 16 warps per set on 16-bit Fisher-Yates maps, or (beyond what
+    // that layout holds) 8 warps on 16-bit maps
+    if (sketch_use_big(F, a0.m) || sketch_fy16_256(F, a0.m)) {
+      const bool big = sketch_use_big(F, a0.m);
+      const int nt = big ? SKETCH_THREADS_BIG : SKETCH_THREADS;
+      const size_t smem = sketch_smem_bytes(F, a0.m, nt, true);
+      if (smem > SMEM_DYN_MAX) return cudaErrorInvalidValue;
+      auto kern = big ? sketch_sets_kernel<F, SKETCH_THREADS_BIG, true>
+                      : sketch_sets_kernel<F, SKETCH_THREADS, true>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
       if (e != cudaSuccess) return e;
-      sketch_sets_kernel<F, SKETCH_THREADS_BIG><<<(unsigned)grid0, SKETCH_THREADS_BIG, smem, st>>>(a);
+      kern<<<(unsigned)grid0, nt, smem, st>>>(a0);
       return cudaGetLastError();
     }
   }
   const SketchArgs& a = a0;
   const int threads = SKETCH_THREADS;
-  const size_t smem = sketch_smem_bytes(F, a.m, threads, a.fy16 != 0);
+  const size_t smem = sketch_smem_bytes(F, a.m, threads);
   if (smem > SMEM_DYN_MAX) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(sketch_sets_kernel<F>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -578,7 +583,6 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
     a.err_flags = flags;
     a.err_set = d_err_set;
     a.T = *tp;
-    a.fy16 = sketch_fy16_256(fam, m) ? 1 : 0;
     // threshold guess m (ln m + c) / W: c = 3 measured best on config 2
     // (2 - 6 % faster PMH2/PMH4 than c = 4; ~5% of sets retry with 4 tg)
     a.tconst = 3.0;
@@ -619,7 +623,8 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
     if (const char* ev = getenv("PMH_SPLIT_CAP")) sp_cap = atoll(ev);
     if (sp_cap > (1LL << 24) / m) sp_cap = (1LL << 24) / m;
     auto split = [&]() -> cudaError_t {
-      const size_t smem = sketch_smem_bytes(fam, m, SKETCH_THREADS, a.fy16 != 0);
+      const bool fy16 = sketch_fy16_256(fam, m);
+      const size_t smem = sketch_smem_bytes(fam, m, SKETCH_THREADS, fy16);
       int dev = 0, sms = 148, per_sm = 1;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -639,11 +644,14 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
       };
       switch (fam) {
         case FAM_PMH1: return go(sketch_split_kernel<FAM_PMH1>);
-        case FAM_PMH2: return go(sketch_split_kernel<FAM_PMH2>);
+        case FAM_PMH2: return fy16 ? go(sketch_split_kernel<FAM_PMH2, true>)
+                                   : go(sketch_split_kernel<FAM_PMH2>);
         case FAM_PMH3: return go(sketch_split_kernel<FAM_PMH3>);
-        case FAM_PMH4: return go(sketch_split_kernel<FAM_PMH4>);
+        case FAM_PMH4: return fy16 ? go(sketch_split_kernel<FAM_PMH4, true>)
+                                   : go(sketch_split_kernel<FAM_PMH4>);
         case FAM_UW3: return go(sketch_split_kernel<FAM_UW3>);
-        default: return go(sketch_split_kernel<FAM_UW4>);
+        default: return fy16 ? go(sketch_split_kernel<FAM_UW4, true>)
+                             : go(sketch_split_kernel<FAM_UW4>);
       }
     };
     const bool do_split = sp_n >= 64 && sp_cap > 0;

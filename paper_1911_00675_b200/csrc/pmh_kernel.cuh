@@ -116,7 +116,7 @@ struct LocalGrab {
 // of line so the register budget of the heavy recurrences does not spill the
 // streaming prefilter loop around it (one call per batch, i.e. per ~4-32
 // prefilter iterations).  Returns true if an element hit a loop cap.
-template <int F>
+template <int F, bool FY16>
 __device__ __forceinline__ bool run_batch(SetCtx& c, const Tables& T, const uint64_t* ids,
                                        const double* w, WarpScratch* wscr, uint32_t* fy_dense,
                                        bool warp_ok, int lane, int take, int qn) {
@@ -146,7 +146,7 @@ __device__ __forceinline__ bool run_batch(SetCtx& c, const Tables& T, const uint
     const int64_t eh = __shfl_sync(0xffffffffu, e, l);
     const uint64_t idh = __ldg(&ids[eh]);
     const double winvh = (family_weighted(F) && w) ? 1.0 / __ldg(&w[eh]) : 1.0;
-    const int st = warp_element<F>(c, T, *wscr, fy_dense, lane, eh, idh, winvh);
+    const int st = warp_element<F, FY16>(c, T, *wscr, fy_dense, lane, eh, idh, winvh);
     if (st == EL_FAIL) failed = true;
     if (lane == 0) c.multi++;
     __syncwarp();
@@ -170,7 +170,7 @@ __device__ __forceinline__ bool run_batch(SetCtx& c, const Tables& T, const uint
 #ifndef PMH_EPL
 #define PMH_EPL 4
 #endif
-template <int F, class Grab>
+template <int F, bool FY16, class Grab>
 __device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const uint64_t* ids,
                                            const double* w, int64_t n, int64_t chunk, Grab& grab,
                                            WarpScratch* wscr, uint32_t* fy_dense, bool warp_ok,
@@ -210,7 +210,7 @@ __device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const 
     }
     while (qn >= 32 || (!more && qn > 0)) {
       const int take = qn < 32 ? qn : 32;
-      if (run_batch<F>(c, T, ids, w, wscr, fy_dense, warp_ok, lane, take, qn)) failed = true;
+      if (run_batch<F, FY16>(c, T, ids, w, wscr, fy_dense, warp_ok, lane, take, qn)) failed = true;
       qn -= take;
       __syncwarp();
     }
@@ -233,7 +233,7 @@ struct SetShared {
 // slot table (in-set element indices); the threshold guess uses the range's
 // own total weight.  Returns true if an element hit a loop cap.  Counters of
 // the range in pts/mul/upd (CTA-reduced, valid in every thread).
-template <int F>
+template <int F, bool FY16>
 __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, int64_t e0,
                                              int64_t e1, Slot* slots, WarpScratch* wscr,
                                              uint32_t* fy_dense, bool warp_ok, SetShared& sh,
@@ -281,7 +281,6 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
   c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
   c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
   c.eoff = e0;
-  c.fy16 = a.fy16 != 0;
   double tg = (double)m * (log((double)m) + a.tconst) / W;
   if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
   bool failed = false;
@@ -293,7 +292,7 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
     if (threadIdx.x == 0) sh.next = 0;
     __syncthreads();
     SharedGrab grab{&sh.next, (unsigned)chunk};
-    warp_elements<F>(c, a.T, ids, w, n, chunk, grab, wscr, fy_dense, warp_ok, failed, lane);
+    warp_elements<F, FY16>(c, a.T, ids, w, n, chunk, grab, wscr, fy_dense, warp_ok, failed, lane);
     __syncthreads();
     // verification: every slot non-empty and <= tguess
     unsigned long long mx = 0;
@@ -328,23 +327,25 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
 #define SKETCH_MINBLOCKS 3   // 80 registers, 3 CTAs/SM: measured 3-12% faster than 2
 #endif
 
-template <int F>
+template <int F, bool FY16>
 __device__ __forceinline__ void sketch_cta_setup(unsigned char* smem, int64_t m, Slot** slots,
-                                                 WarpScratch** wscr, uint32_t** fy_dense,
-                                                 bool fy16) {
+                                                 WarpScratch** wscr, uint32_t** fy_dense) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   *slots = reinterpret_cast<Slot*>(smem);
   *wscr = reinterpret_cast<WarpScratch*>(smem + sizeof(Slot) * m) + wid;
   *fy_dense = reinterpret_cast<uint32_t*>(smem + sizeof(Slot) * m + sizeof(WarpScratch) * nwarps +
-                                          fy_map_bytes(m, fy16) * (size_t)wid);
+                                          fy_map_bytes(m, FY16) * (size_t)wid);
   if (family_uses_fy(F)) {  // epoch 0 never matches: the map starts empty
-    fy_clear(*fy_dense, m, fy16, lane);
+    fy_clear<FY16>(*fy_dense, m, lane);
     if (lane == 0) (*wscr)->epoch = 0;
   }
 }
 
-template <int F, int NT = SKETCH_THREADS>
+// FY16: 16-bit dense Fisher-Yates maps (EpochFY<true>), a compile-time choice
+// so the other instantiations carry no trace of it (these kernels are
+// instruction-cache bound)
+template <int F, int NT = SKETCH_THREADS, bool FY16 = false>
 __global__ void __launch_bounds__(NT, (NT == SKETCH_THREADS ? SKETCH_MINBLOCKS : 1))
     sketch_sets_kernel(SketchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(NT, (NT == SKETCH_THREADS ? SKETCH_MINBLOCKS :
   Slot* slots;
   WarpScratch* wscr;
   uint32_t* fy_dense;
-  sketch_cta_setup<F>(smem, m, &slots, &wscr, &fy_dense, a.fy16 != 0);
+  sketch_cta_setup<F, FY16>(smem, m, &slots, &wscr, &fy_dense);
   // mode B needs static point offsets (power-of-two m) unless the family
   // parses its bit offsets (Fisher-Yates families)
   const bool warp_ok = family_uses_fy(F) || ((m & (m - 1)) == 0);
@@ -372,7 +373,7 @@ __global__ void __launch_bounds__(NT, (NT == SKETCH_THREADS ? SKETCH_MINBLOCKS :
       continue;
     }
     long long pts = 0, mul = 0, upd = 0;
-    const bool failed = sketch_range<F>(a, off, 0, n, slots, wscr, fy_dense, warp_ok, sh, &pts,
+    const bool failed = sketch_range<F, FY16>(a, off, 0, n, slots, wscr, fy_dense, warp_ok, sh, &pts,
                                         &mul, &upd);
     if (failed && threadIdx.x == 0) {
       atomicOr(a.err_flags, (unsigned long long)ERRF_RANDOMNESS);
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(NT, (NT == SKETCH_THREADS ? SKETCH_MINBLOCKS :
 
 // Parts of the split sets (pmh_split.cuh): persistent CTAs, each part's
 // verified minima merged into the set's global table.
-template <int F>
+template <int F, bool FY16 = false>
 __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS)
     sketch_split_kernel(SketchArgs a, SplitArgs sp) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -405,12 +406,12 @@ __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS)
   Slot* slots;
   WarpScratch* wscr;
   uint32_t* fy_dense;
-  sketch_cta_setup<F>(smem, m, &slots, &wscr, &fy_dense, a.fy16 != 0);
+  sketch_cta_setup<F, FY16>(smem, m, &slots, &wscr, &fy_dense);
   const bool warp_ok = family_uses_fy(F) || ((m & (m - 1)) == 0);
   SplitPart p;
   while (split_next_part(sp, &s_t, &p)) {
     long long pts = 0, mul = 0, upd = 0;
-    const bool failed = sketch_range<F>(a, p.off, p.e0, p.e1, slots, wscr, fy_dense, warp_ok, sh,
+    const bool failed = sketch_range<F, FY16>(a, p.off, p.e0, p.e1, slots, wscr, fy_dense, warp_ok, sh,
                                         &pts, &mul, &upd);
     if (failed && threadIdx.x == 0) {
       atomicOr(a.err_flags, (unsigned long long)ERRF_RANDOMNESS);
@@ -516,14 +517,13 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
     c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
     c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
     c.eoff = 0;
-    c.fy16 = false;
     double tg = (double)m * (log((double)m) + a.tconst) / W;
     if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
     bool failed = false;
     for (int attempt = 0;; attempt++) {
       c.tguess = tg;
       LocalGrab grab{0u, 32u * PMH_EPL};
-      warp_elements<F>(c, a.T, ids, w, n, 32 * PMH_EPL, grab, ws, fy, warp_ok, failed, lane);
+      warp_elements<F, false>(c, a.T, ids, w, n, 32 * PMH_EPL, grab, ws, fy, warp_ok, failed, lane);
       unsigned long long mx = 0;
       for (int64_t k = lane; k < m; k += 32) {
         const unsigned long long h = slots[k].h;

@@ -52,7 +52,6 @@ struct SetCtx {
   int64_t multi;                     // elements that produced > 1 point
   int since_refresh;                 // batches since the last h_max refresh
   int64_t eoff;                      // in-set index of element 0 (a split set's part)
-  bool fy16;                         // dense Fisher-Yates maps are 16-bit (EpochFY)
 };
 
 __device__ __forceinline__ double ctx_thr(const SetCtx& c) {
@@ -356,7 +355,6 @@ struct SketchArgs {
   double tconst;            // threshold-guess constant (ln m + tconst)
   const unsigned* counts;   // device: [0] = number of large sets (order prefix)
   const long long* split_info;  // order[0, split_info[0]) are split (pmh_split.cuh)
-  int fy16;                 // 16-bit dense Fisher-Yates maps (sketch_sets_kernel<F, 512>)
 };
 
 __device__ __forceinline__ double block_sum(double v, double* red) {

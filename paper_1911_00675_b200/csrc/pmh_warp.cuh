@@ -46,13 +46,14 @@ struct WarpScratch {
 // | value (m < 8192, epochs 1..7, the map cleared when they wrap): half the
 // shared memory, so large-m sets run 16 warps per CTA (FY_EPOCHS16).
 constexpr uint32_t FY_EPOCHS32 = 0x10000u, FY_EPOCHS16 = 8u;
+template <bool H16>
 struct EpochFY {
+  static constexpr bool h16 = H16;
   uint32_t* a;
   uint32_t ep;
-  bool h16;
   __device__ __forceinline__ int32_t get(int32_t p) const {
     PMH_ASSERT(p >= 0 && p < (h16 ? 8192 : 65536));
-    if (h16) {
+    if constexpr (H16) {
       const uint32_t v = reinterpret_cast<const uint16_t*>(a)[p];
       return (v >> 13) == ep ? (int32_t)(v & 0x1fffu) : p;
     }
@@ -61,14 +62,15 @@ struct EpochFY {
   }
   __device__ __forceinline__ void set(int32_t p, int32_t v) {
     PMH_ASSERT(p >= 0 && v >= 0 && (h16 ? (p < 8192 && v < 8192 && ep < 8) : (p < 65536 && v < 65536)));
-    if (h16) reinterpret_cast<uint16_t*>(a)[p] = (uint16_t)((ep << 13) | (uint32_t)v);
+    if constexpr (H16) reinterpret_cast<uint16_t*>(a)[p] = (uint16_t)((ep << 13) | (uint32_t)v);
     else a[p] = (ep << 16) | (uint32_t)v;
   }
 };
 
 // clear a dense map (entries 0..m) -- epoch 0 never matches
-__device__ __forceinline__ void fy_clear(uint32_t* fy, int64_t m, bool h16, int lane) {
-  if (h16) {
+template <bool H16>
+__device__ __forceinline__ void fy_clear(uint32_t* fy, int64_t m, int lane) {
+  if constexpr (H16) {
     uint16_t* f = reinterpret_cast<uint16_t*>(fy);
     for (int64_t p = lane; p <= m; p += 32) f[p] = 0;
   } else {
@@ -322,11 +324,23 @@ __device__ __forceinline__ uint32_t accept_mask_k(const uint64_t* w, uint32_t po
 template <uint32_t T0, uint32_t T1>
 __device__ __forceinline__ uint32_t accept_mask_sel(const uint64_t* w, uint32_t pos, uint32_t kb,
                                                     uint64_t R, uint32_t fpw) {
+// PMH_ACC_SPEC 2: kb = 6/8/10/12 specialised; 1: 10/12 only; 0: none.
+// Measured (configs[1] PMH2/PMH4 ms, configs[3] PMH2/PMH4, configs[4]):
+// 2: 7.81/5.87, 108.5/83.4, 24.4;  1: 8.06/6.24, 112.6/83.9, 25.8;
+// 0: 7.99/6.22, 93.8/84.2, 26.4 -- the warp-per-set kernel of configs[3] is
+// instruction-cache bound, so results follow code layout more than op counts
+#ifndef PMH_ACC_SPEC
+#define PMH_ACC_SPEC 2
+#endif
   switch (kb) {
+#if PMH_ACC_SPEC >= 2
     case 6: return accept_mask_k<6, T0, T1>(w, pos, (uint32_t)R);
     case 8: return accept_mask_k<8, T0, T1>(w, pos, (uint32_t)R);
+#endif
+#if PMH_ACC_SPEC >= 1
     case 10: return accept_mask_k<10, T0, T1>(w, pos, (uint32_t)R);
     case 12: return accept_mask_k<12, T0, T1>(w, pos, (uint32_t)R);
+#endif
     default: return accept_mask(w, pos, kb, R, T0, T1, fpw);
   }
 }
@@ -419,7 +433,8 @@ __device__ void parse_fy_parallel(const SetCtx& c, WarpScratch& ws, uint64_t id,
 // and each distinct target finally holds the v of its last writer.  Earlier
 // writers come from __match_any_sync; the (short) v chains resolve by shuffle
 // pointer chasing.
-__device__ __forceinline__ void fy_steps_parallel(WarpScratch& ws, EpochFY fy, int64_t i0,
+template <class FYMap>
+__device__ __forceinline__ void fy_steps_parallel(WarpScratch& ws, FYMap fy, int64_t i0,
                                                   uint32_t q, int lane) {
   const bool valid = (uint32_t)lane < q;
   const int32_t pt = (int32_t)(i0 + lane);
@@ -453,18 +468,18 @@ __device__ __forceinline__ void fy_steps_parallel(WarpScratch& ws, EpochFY fy, i
   __syncwarp();
 }
 
-template <int F>
+template <int F, bool FY16>
 __device__ int warp_el_fy(SetCtx& c, const Tables& T, WarpScratch& ws, uint32_t* fy, int lane,
                           int64_t e, uint64_t id, double winv) {
   const int64_t m = c.m;
   uint32_t ep = ws.epoch + 1;
-  if (ep >= (c.fy16 ? FY_EPOCHS16 : FY_EPOCHS32)) {  // epoch wrap: clear the map
-    fy_clear(fy, m, c.fy16, lane);
+  if (ep >= (FY16 ? FY_EPOCHS16 : FY_EPOCHS32)) {  // epoch wrap: clear the map
+    fy_clear<FY16>(fy, m, lane);
     ep = 1;
   }
   __syncwarp();
   if (lane == 0) ws.epoch = ep;
-  EpochFY efy{fy, ep, c.fy16};
+  EpochFY<FY16> efy{fy, ep};
   uint64_t off = 0;
   int64_t i = 1;
   double x = 0.0;
@@ -546,14 +561,14 @@ __device__ int warp_el_fy(SetCtx& c, const Tables& T, WarpScratch& ws, uint32_t*
   }
 }
 
-template <int F>
+template <int F, bool FY16>
 __device__ __forceinline__ int warp_element(SetCtx& c, const Tables& T, WarpScratch& ws,
                                             uint32_t* fy, int lane, int64_t e, uint64_t id,
                                             double winv) {
   if constexpr (F == FAM_PMH1 || F == FAM_PMH3 || F == FAM_UW3)
     return warp_el_static<F>(c, T, ws, lane, e, id, winv);
   else
-    return warp_el_fy<F>(c, T, ws, fy, lane, e, id, winv);
+    return warp_el_fy<F, FY16>(c, T, ws, fy, lane, e, id, winv);
 }
 
 }  // namespace pmh
