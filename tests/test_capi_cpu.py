@@ -167,3 +167,21 @@ def test_nonstreaming_api_validation():
         probminhash4_nonstreaming(ws, 1)           # m >= 2 like probminhash4
     with pytest.raises(EmptyInputError):
         probminhash2_nonstreaming(WeightedSet([]), 16)
+
+
+@pytest.mark.parametrize("algo,m_bad", [("pminhash", 16385), ("minhash", 16385),
+                                        ("probminhash1", 13553), ("probminhash3a", 13553),
+                                        ("unweighted3", 13553), ("probminhash2", 6776),
+                                        ("probminhash4", 6776), ("unweighted4", 6776),
+                                        ("superminhash", 65536)])
+def test_signature_size_limits_rejected_before_cuda(algo, m_bad):
+    """m beyond the shared-memory limits is refused with
+    PMH_ERR_INVALID by host validation -- no CUDA call is made, so this runs
+    without a GPU."""
+    import ctypes
+    from paper_1911_00675_b200 import _lib
+    L = _lib.load()
+    err = ctypes.c_int64(-1)
+    p = ctypes.c_void_p(4096)      # never dereferenced: validation fails first
+    rc = L.pmh_sketch_csr(_lib.ALG[algo], m_bad, p, p, p, 1, p, None, ctypes.byref(err), None)
+    assert rc == _lib.PMH_ERR_INVALID
