@@ -128,15 +128,6 @@ struct SparseFY {
   }
 };
 
-struct DenseFY {  // shared memory, 0 == untouched
-  int32_t* a;
-  __device__ __forceinline__ int32_t get(int32_t p) const {
-    int32_t v = a[p];
-    return v ? v : p;
-  }
-  __device__ __forceinline__ bool set(int32_t p, int32_t v) { a[p] = v; return true; }
-};
-
 // Returns label k (1-based), 0 on FY overflow, -1 on randomness failure.
 template <class FY>
 __device__ __forceinline__ int64_t perm_next(Stream& st, FY& fy, int64_t i,
