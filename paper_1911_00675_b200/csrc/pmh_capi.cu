@@ -985,7 +985,9 @@ namespace {
 template <class Cmp>
 int launch_allpairs_reduce(const uint64_t* rows, int64_t len, int64_t m, Cmp cmp, int64_t r0,
                            int64_t r1, int64_t c0, int64_t c1, int32_t thr, uint64_t* hist,
-                           uint64_t* pairs, int64_t cap, uint64_t* cursor, cudaStream_t st) {
+                           uint64_t* pairs, int64_t cap, uint64_t* cursor, cudaStream_t st,
+                           const unsigned long long* gate = nullptr,
+                           unsigned long long gate_cap = 0) {
   const size_t smem = 2 * sizeof(uint64_t) * AP_KS * (AP_TILE + 1) + sizeof(unsigned) * (size_t)(m + 1);
   PMH_CUDA(cudaFuncSetAttribute(allpairs_reduce_kernel<Cmp>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1000,9 +1002,45 @@ int launch_allpairs_reduce(const uint64_t* rows, int64_t len, int64_t m, Cmp cmp
   if (grid > ntiles) grid = ntiles;
   allpairs_reduce_kernel<Cmp><<<(unsigned)grid, 256, smem, st>>>(
       rows, len, m, cmp, r0, r1, c0, c1, thr, (unsigned long long*)hist,
-      (unsigned long long*)pairs, cap, (unsigned long long*)cursor);
+      (unsigned long long*)pairs, cap, (unsigned long long*)cursor, gate, gate_cap);
   PMH_CUDA(cudaGetLastError());
   return PMH_OK;
+}
+
+// Exact all-pairs counts in two stages (pmh_pminhash.cuh: allpairs_lo_kernel):
+// low-32-bit compares over every pair, exact recount of the pairs with a
+// low-word match, the exact single-stage reduction as a device-gated fallback
+// when the candidate list overflows.  Stream-ordered, no host sync.
+int launch_allpairs_exact2(const uint64_t* sigs, int64_t m, int64_t r0, int64_t r1, int64_t c0,
+                           int64_t c1, int32_t thr, uint64_t* hist, uint64_t* pairs, int64_t cap,
+                           uint64_t* cursor, cudaStream_t st) {
+  const int64_t rows = r1 - r0, cols = c1 - c0;
+  int64_t ccap = rows * cols;                 // upper bound on the range's pairs
+  if (ccap > (1LL << 22)) ccap = 1LL << 22;
+  if (const char* ev = getenv("PMH_ALLPAIRS_CCAP")) ccap = atoll(ev) > 0 ? atoll(ev) : 1;  // tests
+  unsigned long long* tmp = nullptr;          // [zeros, ccursor, cand[ccap]]
+  cudaError_t e = cudaMallocAsync((void**)&tmp, sizeof(unsigned long long) * (size_t)(ccap + 2), st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  PMH_CUDA(cudaMemsetAsync(tmp, 0, 2 * sizeof(unsigned long long), st));
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, allpairs_lo_kernel, 256, 0);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ntiles = ((rows + AP_TILE - 1) / AP_TILE) * ((cols + AP_TILE - 1) / AP_TILE);
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > ntiles) grid = ntiles;
+  allpairs_lo_kernel<<<(unsigned)grid, 256, 0, st>>>(sigs, m, r0, r1, c0, c1, tmp, tmp + 2, ccap,
+                                                     tmp + 1);
+  allpairs_cand_kernel<<<(unsigned)(sms * 8), 256, 0, st>>>(
+      sigs, m, tmp + 2, ccap, tmp + 1, thr, (unsigned long long*)hist,
+      (unsigned long long*)pairs, cap, (unsigned long long*)cursor);
+  allpairs_zeros_kernel<<<1, 32, 0, st>>>(tmp, tmp + 1, ccap, (unsigned long long*)hist);
+  PMH_CUDA(cudaGetLastError());
+  const int rc = launch_allpairs_reduce(sigs, m, m, EqU64{}, r0, r1, c0, c1, thr, hist, pairs, cap,
+                                        cursor, st, tmp + 1, (unsigned long long)ccap);
+  cudaFreeAsync(tmp, st);
+  return rc;
 }
 }  // namespace
 
@@ -1014,8 +1052,12 @@ int pmh_allpairs_hist(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0, in
   if (m < 1 || m > 65535 || r0 < 0 || r1 > n || c0 < 0 || c1 > n || r0 > r1 || c0 > c1)
     return set_error(PMH_ERR_INVALID, "bad tile bounds");
   if (r0 == r1 || c0 == c1) return PMH_OK;
-  return launch_allpairs_reduce(sigs, m, m, EqU64{}, r0, r1, c0, c1, thr, hist, pairs, cap,
-                                cursor, (cudaStream_t)stream);
+  // thr <= 0 lists every pair, zero counts included: single stage
+  if (thr <= 0 || getenv("PMH_ALLPAIRS_1STAGE"))
+    return launch_allpairs_reduce(sigs, m, m, EqU64{}, r0, r1, c0, c1, thr, hist, pairs, cap,
+                                  cursor, (cudaStream_t)stream);
+  return launch_allpairs_exact2(sigs, m, r0, r1, c0, c1, thr, hist, pairs, cap, cursor,
+                                (cudaStream_t)stream);
 }
 
 int64_t pmh_bbit_words(int64_t m, int b) {

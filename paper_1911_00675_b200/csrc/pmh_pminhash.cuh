@@ -607,8 +607,19 @@ __global__ void __launch_bounds__(256) allpairs_tile_kernel(
 // top bit iff its low b-1 bits are nonzero (L = low b-1 bits of every field,
 // H = top bit of every field), nz = (t | x) & H -- so count = m - sum popc.
 // Padding fields are zero in both rows and never counted as unequal.
+// c += (a == b) as a compare and a predicated add (the compiler's own
+// lowering is compare, increment, predicated move: 3 instructions)
+__device__ __forceinline__ void acc_eq32(uint32_t& c, uint32_t a, uint32_t b) {
+  asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}"
+      : "+r"(c) : "r"(a), "r"(b));
+}
+__device__ __forceinline__ void acc_eq64(uint32_t& c, uint64_t a, uint64_t b) {
+  asm("{\n\t.reg .pred p;\n\tsetp.eq.u64 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}"
+      : "+r"(c) : "l"(a), "l"(b));
+}
 struct EqU64 {
   __device__ __forceinline__ uint32_t op(uint64_t a, uint64_t b) const { return a == b; }
+  __device__ __forceinline__ void acc(uint32_t& c, uint64_t a, uint64_t b) const { acc_eq64(c, a, b); }
   __device__ __forceinline__ int64_t finish(uint32_t c) const { return c; }
 };
 struct BBitNeq {
@@ -618,6 +629,7 @@ struct BBitNeq {
     const uint64_t x = a ^ b;
     return (uint32_t)__popcll((((x & L) + L) | x) & H);
   }
+  __device__ __forceinline__ void acc(uint32_t& c, uint64_t a, uint64_t b) const { c += op(a, b); }
   __device__ __forceinline__ int64_t finish(uint32_t c) const { return m - (int64_t)c; }
 };
 // compile-time masks for the common b (the b = 1 case reduces to popc(a ^ b))
@@ -643,6 +655,7 @@ struct BBitNeqT {
       return (uint32_t)__popcll((((x & L) + L) | x) & H);
     }
   }
+  __device__ __forceinline__ void acc(uint32_t& c, uint64_t a, uint64_t b) const { c += op(a, b); }
   __device__ __forceinline__ int64_t finish(uint32_t c) const { return m - (int64_t)c; }
 };
 
@@ -656,7 +669,10 @@ template <class Cmp>
 __global__ void __launch_bounds__(256) allpairs_reduce_kernel(
     const uint64_t* __restrict__ sigs, int64_t len, int64_t m, Cmp cmp, int64_t r0, int64_t r1,
     int64_t c0, int64_t c1, int32_t thr, unsigned long long* __restrict__ hist,
-    unsigned long long* __restrict__ pairs, int64_t cap, unsigned long long* __restrict__ cursor) {
+    unsigned long long* __restrict__ pairs, int64_t cap, unsigned long long* __restrict__ cursor,
+    const unsigned long long* __restrict__ gate = nullptr, unsigned long long gate_cap = 0) {
+  // gate (two-stage exact path): run only when the candidate list overflowed
+  if (gate && *gate <= gate_cap) return;
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t (*sa)[AP_TILE + 1] = reinterpret_cast<uint64_t (*)[AP_TILE + 1]>(smem);
   uint64_t (*sb)[AP_TILE + 1] =
@@ -697,7 +713,7 @@ __global__ void __launch_bounds__(256) allpairs_reduce_kernel(
 #pragma unroll
         for (int u = 0; u < 4; u++)
 #pragma unroll
-          for (int v = 0; v < 4; v++) cnt[u][v] += cmp.op(av[u], bv[v]);
+          for (int v = 0; v < 4; v++) cmp.acc(cnt[u][v], av[u], bv[v]);
       }
     }
 #pragma unroll
@@ -723,6 +739,118 @@ __global__ void __launch_bounds__(256) allpairs_reduce_kernel(
   __syncthreads();
   for (int64_t b = threadIdx.x; b <= m; b += blockDim.x)
     if (shist[b]) atomicAdd(&hist[b], (unsigned long long)shist[b]);
+}
+
+// Two-stage exact all-pairs (EqU64 semantics at about half the ALU work):
+// stage 1 compares only the LOW 32 bits of every component pair.  A pair
+// whose low words never match has an exact count of 0 (counted into *zeros);
+// every other pair is appended to a candidate list (dropped beyond ccap; the
+// cursor still counts them).  Stage 2 recounts the candidates exactly (64-bit
+// compares, warp per pair) into hist / pairs; stage 3 adds the zeros.  If the
+// list overflowed, stages 2-3 do nothing and the gated exact reduction
+// (allpairs_reduce_kernel<EqU64>) recomputes the range instead -- all
+// decided on the device, no host synchronisation.
+constexpr int AP_PAD32 = 4;   // keeps each 4-row group 16-byte aligned (LDS.128)
+__global__ void __launch_bounds__(256) allpairs_lo_kernel(
+    const uint64_t* __restrict__ sigs, int64_t m, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+    unsigned long long* __restrict__ zeros, unsigned long long* __restrict__ cand, int64_t ccap,
+    unsigned long long* __restrict__ ccursor) {
+  __shared__ __align__(16) uint32_t sa[AP_KS][AP_TILE + AP_PAD32];
+  __shared__ __align__(16) uint32_t sb[AP_KS][AP_TILE + AP_PAD32];
+  const int64_t nti = (r1 - r0 + AP_TILE - 1) / AP_TILE, ntj = (c1 - c0 + AP_TILE - 1) / AP_TILE;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  unsigned long long nz = 0;
+  for (int64_t t = blockIdx.x; t < nti * ntj; t += gridDim.x) {
+    const int64_t ti = r0 + (t / ntj) * AP_TILE, tj = c0 + (t % ntj) * AP_TILE;
+    if (tj + AP_TILE <= ti + 1) continue;  // entirely on/below the diagonal
+    uint32_t cnt[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+#pragma unroll
+      for (int v = 0; v < 4; v++) cnt[u][v] = 0;
+    for (int64_t k0 = 0; k0 < m; k0 += AP_KS) {
+      __syncthreads();
+      for (int q = threadIdx.x; q < AP_KS * AP_TILE; q += blockDim.x) {
+        const int r = q / AP_KS, kk = q % AP_KS;
+        const int64_t gi = ti + r, gj = tj + r, k = k0 + kk;
+        // out-of-range words compare equal; those pairs are discarded below
+        sa[kk][r] = (gi < r1 && k < m) ? (uint32_t)__ldg(&sigs[gi * m + k]) : 0u;
+        sb[kk][r] = (gj < c1 && k < m) ? (uint32_t)__ldg(&sigs[gj * m + k]) : 0u;
+      }
+      __syncthreads();
+      const int kn = m - k0 < AP_KS ? (int)(m - k0) : AP_KS;
+#pragma unroll 4
+      for (int kk = 0; kk < kn; kk++) {
+        const uint4 a4 = *reinterpret_cast<const uint4*>(&sa[kk][ty * 4]);
+        const uint4 b4 = *reinterpret_cast<const uint4*>(&sb[kk][tx * 4]);
+        const uint32_t av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+          for (int v = 0; v < 4; v++) acc_eq32(cnt[u][v], av[u], bv[v]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int64_t i = ti + ty * 4 + u;
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        const int64_t j = tj + tx * 4 + v;
+        if (i < r1 && j < c1 && j > i) {
+          if (cnt[u][v] == 0) {
+            nz++;
+          } else {
+            const unsigned long long pos = atomicAdd(ccursor, 1ULL);
+            if ((int64_t)pos < ccap) cand[pos] = ((unsigned long long)i << 32) | (unsigned long long)j;
+          }
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
+  if ((threadIdx.x & 31) == 0 && nz) atomicAdd(zeros, nz);
+}
+
+// stage 2: exact count of each candidate pair (warp per pair)
+__global__ void __launch_bounds__(256) allpairs_cand_kernel(
+    const uint64_t* __restrict__ sigs, int64_t m, const unsigned long long* __restrict__ cand,
+    int64_t ccap, const unsigned long long* __restrict__ ccursor, int32_t thr,
+    unsigned long long* __restrict__ hist, unsigned long long* __restrict__ pairs, int64_t cap,
+    unsigned long long* __restrict__ cursor) {
+  const unsigned long long nc = *ccursor;
+  if (nc > (unsigned long long)ccap) return;           // overflow: the gated fallback runs
+  const int lane = threadIdx.x & 31;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p = wg; p < (int64_t)nc; p += nw) {
+    const unsigned long long ij = cand[p];
+    const int64_t i = (int64_t)(ij >> 32), j = (int64_t)(ij & 0xffffffffULL);
+    const uint64_t* a = sigs + i * m;
+    const uint64_t* b = sigs + j * m;
+    uint32_t c = 0;
+    for (int64_t k = lane; k < m; k += 32) c += (__ldg(&a[k]) == __ldg(&b[k]));
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) {
+      atomicAdd(&hist[c], 1ULL);
+      if ((int32_t)c >= thr) {
+        const unsigned long long pos = atomicAdd(cursor, 1ULL);
+        if ((int64_t)pos < cap) {
+          pairs[2 * pos] = ij;
+          pairs[2 * pos + 1] = (unsigned long long)c;
+        }
+      }
+    }
+  }
+}
+
+// stage 3: the pairs stage 1 proved to have no equal component (thr >= 1
+// only: they are never listed)
+__global__ void allpairs_zeros_kernel(const unsigned long long* __restrict__ zeros,
+                                      const unsigned long long* __restrict__ ccursor, int64_t ccap,
+                                      unsigned long long* __restrict__ hist) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (*ccursor > (unsigned long long)ccap) return;
+  hist[0] += *zeros;
 }
 
 // Fused b-bit reduction + packing (K:851-861 + layout): word w of row s holds

@@ -103,3 +103,59 @@ def test_allpairs_hist_vs_oracle_dense():
         h2, _, _ = allpairs_hist_device(t, r0, min(333, r0 + 64), r0, 333, threshold=1000,
                                         hist=h2)
     np.testing.assert_array_equal(h2.cpu().numpy(), hist.cpu().numpy())
+
+
+def _orc_hist(sigs):
+    full = orc.allpairs(sigs)
+    n, m = sigs.shape
+    iu = np.triu_indices(n, 1)
+    return full, iu, np.bincount(full[iu], minlength=m + 1)
+
+
+def test_allpairs_low_word_collisions_are_recounted_exactly():
+    """Two-stage exact all-pairs: components whose LOW 32 bits collide but
+    whose high words differ must not count (stage 2 recounts candidates with
+    64-bit compares)."""
+    import torch
+    rng = np.random.default_rng(11)
+    n, m = 300, 40
+    lo = rng.integers(0, 3, size=(n, m)).astype(np.uint64)          # heavy low-word collisions
+    hi = rng.integers(0, 2, size=(n, m)).astype(np.uint64)          # ~half of them differ above
+    sigs = (hi << np.uint64(32)) | lo
+    t = torch.from_numpy(sigs.view(np.int64)).cuda()
+    hist, pairs, k = allpairs_hist_device(t, threshold=15, cap=1 << 20)
+    full, iu, exp_hist = _orc_hist(sigs)
+    np.testing.assert_array_equal(hist.cpu().numpy(), exp_hist)
+    exp = {(int(i), int(j)) for i, j in zip(*iu) if full[i, j] >= 15}
+    assert {(int(i), int(j)) for i, j, _ in pairs} == exp and k == len(exp)
+
+
+@pytest.mark.parametrize("ccap", ["1", "100"])
+def test_allpairs_candidate_overflow_falls_back_exactly(monkeypatch, ccap):
+    """A candidate list smaller than the candidates switches, on the device,
+    to the single-stage exact reduction: same histogram and pairs."""
+    import torch
+    rng = np.random.default_rng(5)
+    sigs = rng.integers(0, 4, size=(200, 32)).astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+    t = torch.from_numpy(sigs.view(np.int64)).cuda()
+    monkeypatch.setenv("PMH_ALLPAIRS_CCAP", ccap)
+    hist, pairs, k = allpairs_hist_device(t, threshold=12, cap=1 << 20)
+    full, iu, exp_hist = _orc_hist(sigs)
+    np.testing.assert_array_equal(hist.cpu().numpy(), exp_hist)
+    exp = {(int(i), int(j)) for i, j in zip(*iu) if full[i, j] >= 12}
+    assert {(int(i), int(j)) for i, j, _ in pairs} == exp and k == len(exp)
+
+
+def test_allpairs_threshold_zero_lists_every_pair():
+    """thr <= 0 lists every pair, zero counts included (single-stage path)."""
+    import torch
+    rng = np.random.default_rng(6)
+    sigs = rng.integers(0, 1 << 62, size=(90, 16)).astype(np.uint64)
+    sigs[7] = sigs[3]
+    t = torch.from_numpy(sigs.view(np.int64)).cuda()
+    hist, pairs, k = allpairs_hist_device(t, threshold=0, cap=1 << 20)
+    assert k == 90 * 89 // 2 and len(pairs) == k
+    full, iu, exp_hist = _orc_hist(sigs)
+    np.testing.assert_array_equal(hist.cpu().numpy(), exp_hist)
+    assert {(int(i), int(j), int(c)) for i, j, c in pairs} == \
+        {(int(i), int(j), int(full[i, j])) for i, j in zip(*iu)}
