@@ -536,6 +536,17 @@ __global__ void count_equal_kernel(const uint64_t* __restrict__ A,
   }
 }
 
+// c += (a == b) as a compare and a predicated add (the compiler's own
+// lowering is compare, increment, predicated move: 3 instructions)
+__device__ __forceinline__ void acc_eq32(uint32_t& c, uint32_t a, uint32_t b) {
+  asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}"
+      : "+r"(c) : "r"(a), "r"(b));
+}
+__device__ __forceinline__ void acc_eq64(uint32_t& c, uint64_t a, uint64_t b) {
+  asm("{\n\t.reg .pred p;\n\tsetp.eq.u64 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}"
+      : "+r"(c) : "l"(a), "l"(b));
+}
+
 // All-pairs tile: counts[i - r0][j - c0] for i in [r0,r1), j in [c0,c1) with
 // j > i (upper triangle; other entries untouched).  Signatures are u64 rows;
 // 64x64 pair tile per CTA, components staged through shared memory in
@@ -554,7 +565,7 @@ __global__ void __launch_bounds__(256) allpairs_tile_kernel(
   if (ti >= r1 || tj >= c1) return;
   if (tj + AP_TILE <= ti + 1) return;  // tile entirely on/below the diagonal
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16x16 threads, 4x4 pairs each
-  int cnt[4][4];
+  uint32_t cnt[4][4];
 #pragma unroll
   for (int u = 0; u < 4; u++)
 #pragma unroll
@@ -578,7 +589,7 @@ __global__ void __launch_bounds__(256) allpairs_tile_kernel(
 #pragma unroll
       for (int u = 0; u < 4; u++)
 #pragma unroll
-        for (int v = 0; v < 4; v++) cnt[u][v] += (av[u] == bv[v]);
+        for (int v = 0; v < 4; v++) acc_eq64(cnt[u][v], av[u], bv[v]);
     }
   }
 #pragma unroll
@@ -607,16 +618,6 @@ __global__ void __launch_bounds__(256) allpairs_tile_kernel(
 // top bit iff its low b-1 bits are nonzero (L = low b-1 bits of every field,
 // H = top bit of every field), nz = (t | x) & H -- so count = m - sum popc.
 // Padding fields are zero in both rows and never counted as unequal.
-// c += (a == b) as a compare and a predicated add (the compiler's own
-// lowering is compare, increment, predicated move: 3 instructions)
-__device__ __forceinline__ void acc_eq32(uint32_t& c, uint32_t a, uint32_t b) {
-  asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}"
-      : "+r"(c) : "r"(a), "r"(b));
-}
-__device__ __forceinline__ void acc_eq64(uint32_t& c, uint64_t a, uint64_t b) {
-  asm("{\n\t.reg .pred p;\n\tsetp.eq.u64 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}"
-      : "+r"(c) : "l"(a), "l"(b));
-}
 struct EqU64 {
   __device__ __forceinline__ uint32_t op(uint64_t a, uint64_t b) const { return a == b; }
   __device__ __forceinline__ void acc(uint32_t& c, uint64_t a, uint64_t b) const { acc_eq64(c, a, b); }
