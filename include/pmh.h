@@ -163,7 +163,11 @@ int pmh_allpairs_tile(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0,
  * hist[c] (uint64[m+1], caller-zeroed) the number of pairs with c equal
  * components, and appends every pair with count >= thr to pairs as
  * {(i << 32) | j, count} (uint64[2*cap]); *cursor (caller-zeroed uint64)
- * ends at the number of such pairs (entries beyond cap are dropped).
+ * ends at the number of such pairs (entries beyond cap are dropped; the
+ * order of the list is unspecified).  thr >= 1 runs two exact stages (low-
+ * word compares over every pair, 64-bit recount of the pairs with a low-word
+ * match; a stream-ordered temporary of up to 32 MB from the device pool);
+ * thr <= 0 lists every pair in one stage.
  */
 int pmh_allpairs_hist(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0, int64_t r1,
                       int64_t c0, int64_t c1, int32_t thr, uint64_t* hist, uint64_t* pairs,
