@@ -552,7 +552,7 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
                         split_cap > 0;
   OrderWs ow;
   // cost offset: ProbMinHash families pay ~m ln m points per set regardless of n
-  e = build_order(offsets, nsets, pmin ? 0 : (int64_t)(PMH_ORDER_COST_M * (double)m), pmin ? -1 : small_n_for(m),
+  e = build_order(offsets, nsets, pmin ? 0 : (int64_t)(PMH_ORDER_COST_M * (double)m), pmin ? -1 : small_n_for(fam, m),
                   pm_split ? split_n : 4096, st, &ow);
   if (e != cudaSuccess) return cuda_fail(e, "set ordering");
   int32_t* order = ow.order;

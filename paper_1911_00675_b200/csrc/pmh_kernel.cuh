@@ -447,14 +447,22 @@ namespace pmh {
 #ifndef PMH_SMALL_N
 #define PMH_SMALL_N 3
 #endif
-constexpr int64_t SMALL_N = PMH_SMALL_N;   // sets up to this size run warp-per-set (measured)
+#ifndef PMH_SMALL_N_STATIC
+#define PMH_SMALL_N_STATIC 7
+#endif
+// sets up to this size run warp-per-set at large m (measured on configs[1]:
+// cutoff 7 vs 3 is 2% / 6% faster for ProbMinHash 1 / 3 and 4% slower for
+// the Fisher-Yates families 2 / 4, whose warp-per-set map costs more)
+constexpr int64_t SMALL_N = PMH_SMALL_N;
+constexpr int64_t SMALL_N_STATIC = PMH_SMALL_N_STATIC;
 #ifndef PMH_SMALL_N_SMALLM
 #define PMH_SMALL_N_SMALLM 512
 #endif
 // warp-per-set cutoff: for m <= 256 whole sets of up to 512 elements are cheap
 // enough for one warp (configs[3], configs[4]); for large m only tiny sets
-__host__ __device__ inline int64_t small_n_for(int64_t m) {
-  return m <= 256 ? (int64_t)PMH_SMALL_N_SMALLM : SMALL_N;
+__host__ __device__ inline int64_t small_n_for(int family, int64_t m) {
+  if (m <= 256) return (int64_t)PMH_SMALL_N_SMALLM;
+  return family_uses_fy(family) ? SMALL_N : SMALL_N_STATIC;
 }
 
 struct WarpSetVars {
