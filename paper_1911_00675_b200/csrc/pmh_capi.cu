@@ -583,9 +583,11 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
     a.err_flags = flags;
     a.err_set = d_err_set;
     a.T = *tp;
-    // threshold guess m (ln m + c) / W: c = 3 measured best on config 2
-    // (2 - 6 % faster PMH2/PMH4 than c = 4; ~5% of sets retry with 4 tg)
-    a.tconst = 3.0;
+    // threshold guess m (ln m + c) / W, measured on config 2 (c = 2/3/4/5):
+    // c = 3 best for ProbMinHash 1/2/4 (2-6 % faster PMH2/PMH4 than c = 4;
+    // ~5% of sets retry with 4 tg), c = 4 for ProbMinHash 3 (-3% vs 3)
+    a.tconst = fam == FAM_PMH3 ? 4.0 : 3.0;
+    if (const char* ev = getenv("PMH_TCONST")) a.tconst = atof(ev);   // tuning hook
     a.counts = ow.counts;
     // small sets run warp-per-set on the auxiliary stream, concurrently with
     // the CTA-per-set kernel on `st` (fork/join with events)
