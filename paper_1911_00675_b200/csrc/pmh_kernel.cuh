@@ -167,9 +167,7 @@ __device__ __forceinline__ bool run_batch(SetCtx& c, const Tables& T, const uint
 // L2 (prefetched per set) and the weights too (the weight sum), so no
 // register prefetch is kept across the heavy batch.  32-bit element indices
 // (sets hold < 2^31 elements); rejections counted in a register (stats only).
-#ifndef PMH_EPL
-#define PMH_EPL 4
-#endif
+// (PMH_EPL is defined in pmh_warp.cuh next to the queue it sizes)
 template <int F, bool FY16, class Grab>
 __device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const uint64_t* ids,
                                            const double* w, int64_t n, int64_t chunk, Grab& grab,
@@ -202,7 +200,7 @@ __device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const 
         const bool surv = act[j] && !first_point_rejects<F>(T, id[j], wv[j], thr);
         rej += act[j] && !surv;
         const unsigned sm = __ballot_sync(0xffffffffu, surv);
-        PMH_ASSERT(qn + __popc(sm) <= 160);
+        PMH_ASSERT(qn + __popc(sm) <= SQ_CAP);
         if (surv) wscr->sq[qn + __popc(sm & ((1u << lane) - 1u))] = (int32_t)(base + (uint32_t)lane + 32u * j);
         qn += __popc(sm);
       }

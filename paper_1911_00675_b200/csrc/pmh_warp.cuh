@@ -26,6 +26,13 @@ namespace pmh {
 
 constexpr uint32_t WIN_BITS = 2048;  // 32 words
 
+// elements per lane per chunk of the streaming loop (pmh_kernel.cuh); the
+// survivor queue holds < 32 leftovers plus one chunk: 32 * (PMH_EPL + 1)
+#ifndef PMH_EPL
+#define PMH_EPL 4
+#endif
+constexpr int SQ_CAP = 32 * (PMH_EPL + 1);
+
 struct WarpScratch {
   uint64_t words[65];   // window (64 words for the parallel FY parse, +1 guard)
   uint32_t eoff[32];    // window-relative bit offset of each point's first draw
@@ -36,7 +43,7 @@ struct WarpScratch {
   uint64_t next_off;    // absolute bit offset after the batch
   uint32_t epoch;       // Fisher-Yates map epoch (one per warp-processed element)
   uint32_t pad;
-  int32_t sq[160];      // survivor queue of the large-set path (element indices, LIFO)
+  int32_t sq[SQ_CAP];   // survivor queue of the large-set path (element indices, LIFO)
   uint32_t gm[32];      // parallel Fisher-Yates: lanes whose target is i0 + k
 };
 
