@@ -367,7 +367,8 @@ __device__ __forceinline__ void pm64_range(const PMinArgs& a, int64_t off, int64
         // overflow runs them in place.  The threshold refresh is periodic --
         // a stale, larger tmax only admits more candidates.
         const bool inf = !(tmax < 1e300);
-        if (use_q) {
+        // most warp-steps of a large set have no candidate at all: skip the scan
+        if (use_q && __any_sync(0xffffffffu, cand != 0ULL)) {
           const int c = __popcll(cand);
           int x = c;                                   // inclusive lane scan
 #pragma unroll
@@ -394,7 +395,7 @@ __device__ __forceinline__ void pm64_range(const PMinArgs& a, int64_t off, int64
               pm64_check_entry<EXPO>(en, ids, ws, tpg, table);
             }
           }
-        } else if (cand) {
+        } else if (!use_q && cand) {
           pm64_candidates<EXPO>(cand, id, w, (uint32_t)e, t, tpg, table);
         }
         if (++since >= PM64_REFRESH || (cand && inf)) {
