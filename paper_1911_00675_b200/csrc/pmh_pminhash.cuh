@@ -183,7 +183,10 @@ __global__ void __launch_bounds__(PMIN_THREADS) pminhash_kernel(PMinArgs a) {
 // ---------------------------------------------------------------------------
 constexpr int PM64_C = 64;
 #ifndef PM64_REFRESH
-#define PM64_REFRESH 16    // elements between threshold refreshes
+// elements between threshold refreshes (configs[1], after the candidate-scan
+// skip: 8 / 16 / 32 / 64 / 128 -> 74.2 / 72.6 / 71.9 / 71.5 / 71.4 ms; the
+// threshold only moves slowly below its guess, so fresher is not better)
+#define PM64_REFRESH 64
 #endif
 #ifndef PM64_TCONST
 #define PM64_TCONST 8.0    // threshold guess (ln m + c) / W
