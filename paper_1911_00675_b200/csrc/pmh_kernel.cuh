@@ -18,7 +18,7 @@ namespace pmh {
 #define PMH_CHUNK_DIV 2       // element chunks per warp and set (at least)
 #endif
 #ifndef PMH_REFRESH_EVERY
-#define PMH_REFRESH_EVERY 8   // batches between forced h_max refreshes
+#define PMH_REFRESH_EVERY 16  // batches between forced h_max refreshes (4 / 8 / 16: equal within 1%)
 #endif
 #ifndef PMH_HEAVY_POINTS
 #define PMH_HEAVY_POINTS 16.0   // measured best on config 2 (4 / 6 / 8 / 12 / 16 / 24 / 32 / 48 tried)
@@ -151,8 +151,16 @@ __device__ __forceinline__ bool run_batch(SetCtx& c, const Tables& T, const uint
     if (lane == 0) c.multi++;
     __syncwarp();
   }
-  // refresh h_max after batches that lowered a slot (and every 8th)
-  const bool changed = __any_sync(0xffffffffu, c.updates != upd0);
+  // periodic h_max refresh (every PMH_REFRESH_EVERY batches)
+// h_max is kept exact where it matters -- a lowered maximum slot or the last
+// slot filling triggers a recompute (ctx_offer, offer_trig) -- so the warp
+// scan of all m slots after every batch that lowered ANY slot was redundant
+// (configs[1]: PMH1 -7%, PMH2/PMH4 -3%, PMH3 -4% without it); only the
+// periodic safety refresh remains
+#ifndef PMH_REFRESH_ON_CHANGE
+#define PMH_REFRESH_ON_CHANGE 0
+#endif
+  const bool changed = PMH_REFRESH_ON_CHANGE && __any_sync(0xffffffffu, c.updates != upd0);
   if (changed || ++c.since_refresh >= PMH_REFRESH_EVERY) {
     hmax_refresh_warp(c, lane);
     c.since_refresh = 0;
