@@ -161,7 +161,9 @@ __device__ __forceinline__ bool run_batch(SetCtx& c, const Tables& T, const uint
 #define PMH_REFRESH_ON_CHANGE 0
 #endif
   const bool changed = PMH_REFRESH_ON_CHANGE && __any_sync(0xffffffffu, c.updates != upd0);
-  if (changed || ++c.since_refresh >= PMH_REFRESH_EVERY) {
+  const bool trig = __any_sync(0xffffffffu, c.trig);
+  c.trig = false;
+  if (changed || trig || ++c.since_refresh >= PMH_REFRESH_EVERY) {
     hmax_refresh_warp(c, lane);
     c.since_refresh = 0;
   }
@@ -286,6 +288,7 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
   c.kbits = bits_for(m);
   c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
   c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
+  c.trig = false;
   c.eoff = e0;
   double tg = (double)m * (log((double)m) + a.tconst) / W;
   if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
@@ -530,6 +533,7 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
     c.kbits = bits_for(m);
     c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
     c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
+  c.trig = false;
     c.eoff = 0;
     double tg = (double)m * (log((double)m) + a.tconst) / W;
     if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);

@@ -51,6 +51,8 @@ struct SetCtx {
   int64_t updates;
   int64_t multi;                     // elements that produced > 1 point
   int since_refresh;                 // batches since the last h_max refresh
+  bool trig;                         // this lane lowered the maximum slot / filled the last
+                                     // one: the warp refreshes h_max after the batch
   int64_t eoff;                      // in-set index of element 0 (a split set's part)
 };
 
@@ -59,28 +61,20 @@ __device__ __forceinline__ double ctx_thr(const SetCtx& c) {
   return h < c.tguess ? h : c.tguess;
 }
 
-// serial exact recompute of max_k h_k (rare: triggered when the last empty
-// slot fills or when the slot holding the maximum is lowered)
-__device__ __noinline__ void hmax_recompute_serial(SetCtx& c) {
-  unsigned long long mx = 0;
-  for (int64_t k = 0; k < c.m; k++) {
-    unsigned long long h = *(volatile unsigned long long*)&c.slots[k].h;
-    mx = h > mx ? h : mx;
-  }
-  atomicMin(c.hmax_bits, mx);
-}
-
 __device__ __forceinline__ void ctx_offer(SetCtx& c, int64_t k0, double x,
                                           int64_t e) {
   PMH_ASSERT(k0 >= 0 && k0 < c.m);
   unsigned long long prev = slot_offer(&c.slots[k0], x, (unsigned long long)(e + c.eoff));
   if (prev == ~0ULL) return;
   c.updates++;
+  // h_max stays an upper bound of max_k h_k (a valid, if stale, threshold);
+  // the converged warp recomputes it cooperatively after the batch
+  // (run_batch) instead of one lane scanning all m slots here
   if (prev == EMPTY_H) {
     unsigned f = atomicAdd(c.filled, 1u) + 1u;
-    if (f == (unsigned)c.m) hmax_recompute_serial(c);
+    if (f == (unsigned)c.m) c.trig = true;
   } else if (prev >= *(volatile unsigned long long*)c.hmax_bits) {
-    hmax_recompute_serial(c);
+    c.trig = true;
   }
 }
 
