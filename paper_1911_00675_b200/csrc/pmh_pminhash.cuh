@@ -191,7 +191,10 @@ constexpr int PM64_C = 64;
 #ifndef PM64_TCONST
 #define PM64_TCONST 8.0    // threshold guess (ln m + c) / W
 #endif
-constexpr int PM64_CQ = 128;       // queued candidates per warp
+#ifndef PM64_CQ_SIZE
+#define PM64_CQ_SIZE 128   // 64 / 128 / 256: equal within 0.2% on configs[1]
+#endif
+constexpr int PM64_CQ = PM64_CQ_SIZE;   // queued candidates per warp
 
 // Shared table layout: component k = 64 t + q (thread t, draw q) lives at
 // TRANSPOSED index q * tpg + t, so the 16..32 threads of a warp touch
