@@ -120,6 +120,25 @@ struct SparseFY {
     pos[cnt] = p; val[cnt] = v; cnt++;
     return true;
   }
+  // one lazy Fisher-Yates step (K:222-235) in ONE scan: returns perm[j] and
+  // sets perm[j] = perm[i] (both read before the write, as in get/set);
+  // 0 on overflow
+  __device__ __forceinline__ int32_t swap_step(int32_t i, int32_t j) {
+    int32_t vi = i, vj = j;
+    int qj = -1;
+    for (int q = 0; q < cnt; q++) {
+      const int32_t p = pos[q];
+      if (p == j) { vj = val[q]; qj = q; }
+      if (p == i) vi = val[q];
+    }
+    if (qj >= 0) {
+      val[qj] = vi;
+    } else {
+      if (cnt == SPARSE_FY_CAP) return 0;
+      pos[cnt] = j; val[cnt] = vi; cnt++;
+    }
+    return vj;
+  }
 };
 
 // Returns label k (1-based), 0 on FY overflow, -1 on randomness failure.
@@ -128,10 +147,7 @@ __device__ __forceinline__ int64_t perm_next(Stream& st, FY& fy, int64_t i,
                                              int64_t m) {
   int64_t r = uniform_int(st, m - i + 1);
   if (r < 0) return -1;
-  int32_t j = (int32_t)(i + r);
-  int32_t k = fy.get(j);
-  if (!fy.set(j, fy.get((int32_t)i))) return 0;
-  return k;
+  return fy.swap_step((int32_t)i, (int32_t)(i + r));
 }
 
 // result codes of the element processors
