@@ -109,17 +109,6 @@ struct SparseFY {
   int32_t val[SPARSE_FY_CAP];
   int cnt;
   __device__ __forceinline__ void reset() { cnt = 0; }
-  __device__ __forceinline__ int32_t get(int32_t p) const {
-    for (int q = 0; q < cnt; q++) if (pos[q] == p) return val[q];
-    return p;
-  }
-  // returns false on overflow
-  __device__ __forceinline__ bool set(int32_t p, int32_t v) {
-    for (int q = 0; q < cnt; q++) if (pos[q] == p) { val[q] = v; return true; }
-    if (cnt == SPARSE_FY_CAP) return false;
-    pos[cnt] = p; val[cnt] = v; cnt++;
-    return true;
-  }
   // one lazy Fisher-Yates step (K:222-235) in ONE scan: returns perm[j] and
   // sets perm[j] = perm[i] (both read before the write, as in get/set);
   // 0 on overflow
