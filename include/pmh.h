@@ -228,6 +228,27 @@ int64_t pmh_parse_weighted_text(const char* buf, int64_t len, uint64_t* ids, dou
  */
 int pmh_probe_alu_peak(double* gops_out, double* ms_out);
 
+/* Pipe-peak microbenchmark of one instruction kind (0 = LOP3 / 32-bit ALU
+ * pipe, 1 = IMAD / integer multiply-add, 2 = DFMA / FP64 pipe, 3 = FFMA / the
+ * issue-slot ceiling): 8 independent chains per thread at full occupancy,
+ * best of 5 launches on the legacy stream.  Thread-level ops per second in
+ * *gops_out (10^9), the launch time in *ms_out.  Synchronous. */
+int pmh_probe_pipe_peak(int kind, double* gops_out, double* ms_out);
+
+/* Per-point work probe (csrc/pmh_probe.cuh): points/s (10^9) of a tight
+ * loop generating ProbMinHash points with one splitmix64 word, the value
+ * (kind 0: log1p, the ProbMinHash1/2 point; kind 1: TruncExp fast path, the
+ * ProbMinHash3/4 point) and a 128-bit CAS offer into a shared 1024-slot
+ * table, at full occupancy.  The practical point-rate ceiling that bench.py's
+ * per-variant roofline divides by.  Synchronous. */
+int pmh_probe_point_rate(int kind, double* gpts_out, double* ms_out);
+
+/* The device build of the glibc log1p (fn 0) / expm1 (fn 1) restatements the
+ * kernels use (csrc/pmh_math.cuh; reference K:120-122, K:146), evaluated on n
+ * DEVICE doubles x into out (expm1: NaN where it reports no result).
+ * Stream-ordered.  For parity tests of the transcendental itself. */
+int pmh_math_eval(int fn, const double* x, int64_t n, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

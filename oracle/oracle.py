@@ -64,6 +64,9 @@ def lib():
                                          _i64p, ctypes.c_int64, ctypes.c_int64,
                                          _u64p, _i64p]
             L.orc_sketch_csr.restype = ctypes.c_int
+            L.orc_pminhash_part.argtypes = [_u64p, _f64p, ctypes.c_int64, ctypes.c_int64,
+                                            ctypes.c_int64, _f64p, _i64p]
+            L.orc_pminhash_part.restype = None
             L.orc_bbit.argtypes = [_u64p, ctypes.c_int64, ctypes.c_int, _i64p]
             L.orc_count_equal.argtypes = [_u64p, _u64p, ctypes.c_int64,
                                           ctypes.c_int64, _i32p]
@@ -140,6 +143,52 @@ def sketch_csr(algo, m, ids, weights, offsets, set_range=None, threads=1):
         if rc:
             raise OracleError(f"oracle error {rc}")
     return sig, stats
+
+
+def sketch_csr_balanced(algo, m, ids, weights, offsets, threads=1, part=2048):
+    """sketch_csr with equal-cost work items for a multi-core CPU baseline:
+    P-MinHash sets are cut into element parts of <= `part` elements (merged on
+    (h, index): order-independent, so the signature is exactly the sequential
+    one), every other algorithm runs whole sets; items go to the thread pool
+    largest-cost first (LPT).  Returns sig u64[nsets, m]."""
+    ids = np.ascontiguousarray(ids, np.uint64)
+    w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    offsets = np.ascontiguousarray(offsets, np.int64)
+    ns = offsets.size - 1
+    sig = np.zeros((ns, m), np.uint64)
+    L = lib()
+    aid = _algo_id(algo)
+    sizes = np.diff(offsets)
+    if aid == ALG["pminhash"]:
+        items = [(s, a, min(a + part, int(sizes[s]))) for s in range(ns)
+                 for a in range(0, int(sizes[s]), part)]
+        hmin = [np.full((len(range(0, int(sizes[s]), part)), m), np.inf) for s in range(ns)]
+        idx = [np.full((len(range(0, int(sizes[s]), part)), m), -1, np.int64) for s in range(ns)]
+
+        def run(it):
+            s, a, b = it
+            o = int(offsets[s])
+            L.orc_pminhash_part(_p(ids[o + a:], _u64p), _p(w[o + a:], _f64p), b - a, m, a,
+                                _p(hmin[s][a // part], _f64p), _p(idx[s][a // part], _i64p))
+            return 0
+        order = sorted(items, key=lambda it: -(it[2] - it[1]))
+    else:
+        def run(s):
+            return L.orc_sketch_csr(aid, m, _p(ids, _u64p), None if w is None else _p(w, _f64p),
+                                    _p(offsets, _i64p), s, s + 1, _p(sig[s:], _u64p), None)
+        order = sorted(range(ns), key=lambda s: -(int(sizes[s]) + 7 * m))
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        rcs = list(ex.map(run, order))
+    if any(rcs):
+        raise OracleError(f"oracle error {max(rcs)}")
+    if aid == ALG["pminhash"]:
+        for s in range(ns):
+            h, ix = hmin[s], idx[s]
+            # lexicographic (h, index) minimum over the parts of each component
+            best = np.lexsort((ix, h), axis=0)[0]
+            sel = ix[best, np.arange(m)]
+            sig[s] = ids[int(offsets[s]) + sel]
+    return sig
 
 
 def bbit(sig, b):

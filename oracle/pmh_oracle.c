@@ -816,6 +816,25 @@ int orc_sketch_csr(int algo, i64 m, const u64 *ids, const double *w,
     return 0;
 }
 
+/* P-MinHash (K:284-300) over one element range of a set, for the balanced
+ * CPU baseline: folds elements [0, n) (global in-set indices e0 + e) into the
+ * caller's running minima hmin[m] / idx[m] (init +inf / -1).  P-MinHash is
+ * order-independent: the reference's strict `<` in element order keeps the
+ * lexicographic minimum of (h, index), so parts merged on (h, index) give
+ * exactly the sequential signature.                                          */
+void orc_pminhash_part(const u64 *ids, const double *w, i64 n, i64 m, i64 e0,
+                       double *hmin, i64 *idx) {
+    stream_t st;
+    for (i64 e = 0; e < n; e++) {
+        rng_seed(&st, ids[e]);
+        double winv = 1.0 / w[e];
+        for (i64 k = 0; k < m; k++) {
+            double h = winv * exp1(&st);
+            if (h < hmin[k]) { hmin[k] = h; idx[k] = e0 + e; }
+        }
+    }
+}
+
 /* b-bit reduction K:851-861 */
 void orc_bbit(const u64 *sig, i64 m, int b, i64 *out) {
     u64 mask = (1ULL << (u64)b) - 1ULL;

@@ -60,6 +60,46 @@ def to_device_i64(x, device=None):
     return torch.from_numpy(np.ascontiguousarray(x, np.int64)).to(device or "cuda")
 
 
+def _check_host_csr(ids, weights, offsets):
+    """Host CSR bounds: offsets[0] == 0 and offsets[-1] == ids.size (== weights.size
+    when weighted), so the C ABI's copies stay inside the caller's arrays."""
+    if offsets.ndim != 1 or offsets.size < 1:
+        raise InvalidParamsError("offsets must be a 1-d array of nsets + 1 entries")
+    if offsets.size > 1:
+        if int(offsets[0]) != 0:
+            raise InvalidParamsError("offsets[0] must be 0")
+        if int(offsets[-1]) != ids.size:
+            raise InvalidParamsError(f"offsets[-1] = {int(offsets[-1])} != len(ids) = {ids.size}")
+        if weights is not None and weights.size != ids.size:
+            raise InvalidParamsError(f"len(weights) = {weights.size} != len(ids) = {ids.size}")
+
+
+def _check_device_csr(torch, ids, weights, offsets):
+    """Device CSR: dtypes, contiguity, one device, and the offsets' ends against
+    the array lengths (one 16-byte read of offsets; the call syncs anyway)."""
+    if ids.dtype not in (torch.int64, torch.uint64):
+        raise InvalidParamsError(f"ids must be int64/uint64, got {ids.dtype}")
+    if offsets.dtype != torch.int64:
+        raise InvalidParamsError(f"offsets must be int64, got {offsets.dtype}")
+    if weights is not None and weights.dtype != torch.float64:
+        raise InvalidParamsError(f"weights must be float64, got {weights.dtype}")
+    for name, t in (("ids", ids), ("offsets", offsets), ("weights", weights)):
+        if t is None:
+            continue
+        if not t.is_cuda or t.device != ids.device:
+            raise InvalidParamsError(f"{name} must be a CUDA tensor on {ids.device}")
+        if t.dim() != 1 or not t.is_contiguous():
+            raise InvalidParamsError(f"{name} must be a contiguous 1-d tensor")
+    if offsets.numel() > 1:
+        o0, o1 = (int(v) for v in offsets[[0, -1]].tolist())
+        if o0 != 0:
+            raise InvalidParamsError("offsets[0] must be 0")
+        if o1 != ids.numel():
+            raise InvalidParamsError(f"offsets[-1] = {o1} != len(ids) = {ids.numel()}")
+        if weights is not None and weights.numel() != ids.numel():
+            raise InvalidParamsError(f"len(weights) = {weights.numel()} != len(ids) = {ids.numel()}")
+
+
 def _stream_ptr(torch, dev):
     return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
@@ -78,6 +118,7 @@ def sketch_csr_device(algo, m: int, ids, weights, offsets, want_stats=True):
     stats = torch.empty((max(nsets, 0), 3), dtype=torch.int64, device=dev) if want_stats else None
     if aid in _lib.UNWEIGHTED_IDS:
         weights = None
+    _check_device_csr(torch, ids, weights, offsets)
     err = ctypes.c_int64(-1)
     rc = _lib.load().pmh_sketch_csr(
         aid, m, ids.data_ptr(), weights.data_ptr() if weights is not None else None,
@@ -95,6 +136,9 @@ def sketch_csr_multi_device(algos, m: int, ids, weights, offsets, want_stats=Fal
     aids = [algo_id(a) for a in algos]
     nsets = offsets.numel() - 1
     dev = ids.device
+    if all(a in _lib.UNWEIGHTED_IDS for a in aids):
+        weights = None
+    _check_device_csr(torch, ids, weights, offsets)
     sigs = [torch.empty((max(nsets, 0), m), dtype=torch.int64, device=dev) for _ in aids]
     stats = [torch.empty((max(nsets, 0), 3), dtype=torch.int64, device=dev) if want_stats
              else None for _ in aids]
@@ -128,6 +172,7 @@ def sketch_csr(algo, m: int, ids, weights, offsets, want_stats=True):
         w = None
     else:
         w = np.ascontiguousarray(weights, np.float64)
+    _check_host_csr(ids, w, offsets)
     sig = np.empty((max(nsets, 0), m), np.uint64)
     stats = np.empty((max(nsets, 0), 3), np.int64) if want_stats else None
     err = ctypes.c_int64(-1)
@@ -151,6 +196,7 @@ def sketch_csr_multi(algos, m: int, ids, weights, offsets, sig_outs=None, want_s
     offsets = np.ascontiguousarray(offsets, np.int64)
     w = None if weights is None else np.ascontiguousarray(weights, np.float64)
     nsets = offsets.size - 1
+    _check_host_csr(ids, w, offsets)
     if sig_outs is None:
         sig_outs = [np.empty((nsets, m), np.uint64) for _ in algos]
     stats = [np.empty((nsets, 3), np.int64) for _ in algos] if want_stats else None

@@ -111,8 +111,34 @@ int get_tables(int family, int64_t m, const Tables** out) {
     dt.t.gam = (const double*)(p + bc);
     dt.t.dgam = (const double*)(p + bc + bg);
   }
+  // the uploads above are synchronous copies from pageable memory, which may
+  // return before the DMA lands; the kernels that read the tables run on
+  // non-blocking streams that nothing orders after it, so wait here (once per
+  // device, family and m) before publishing the table
+  if (dt.mem) PMH_CUDA(cudaDeviceSynchronize());
   auto res = g_tables.emplace(key, dt);
   *out = &res.first->second.t;
+  return PMH_OK;
+}
+
+// Test hook: PMH_TEST_REJECT_CAP / PMH_TEST_COUPON_CAP lower the device loop
+// caps (pmh_device.cuh) so a test can drive RandomnessFailureError; read once
+// per device.  Unset (always, outside tests) the reference caps apply.
+std::map<int, bool> g_caps_applied;
+int apply_test_caps() {
+  int dev = 0;
+  PMH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_caps_applied[dev]) return PMH_OK;
+  if (const char* ev = getenv("PMH_TEST_REJECT_CAP")) {
+    const int v = atoi(ev);
+    PMH_CUDA(cudaMemcpyToSymbol(g_reject_cap, &v, sizeof(v)));
+  }
+  if (const char* ev = getenv("PMH_TEST_COUPON_CAP")) {
+    const long long v = atoll(ev);
+    PMH_CUDA(cudaMemcpyToSymbol(g_coupon_cap_override, &v, sizeof(v)));
+  }
+  g_caps_applied[dev] = true;
   return PMH_OK;
 }
 
@@ -260,10 +286,25 @@ void ensure_pool_retained() {
   g_pool_set[dev] = true;
 }
 
+// A fork event private to one call: the shared per-device streams below may be
+// used by several host threads at once (ctypes releases the GIL), so the
+// event that orders a shared stream after the CALLER's stream must not be
+// shared -- another thread's record could land between this call's record and
+// its wait.  (Join events are recorded on the shared stream itself, where a
+// later record only waits for more of the same stream: still correct.)
+// Destroying it right after the wait is legal; the wait keeps its snapshot.
+struct ForkEvent {
+  cudaEvent_t e = nullptr;
+  ForkEvent() { cudaEventCreateWithFlags(&e, cudaEventDisableTiming); }
+  ~ForkEvent() { if (e) cudaEventDestroy(e); }
+  ForkEvent(const ForkEvent&) = delete;
+  ForkEvent& operator=(const ForkEvent&) = delete;
+};
+
 // per-device auxiliary stream + events for the concurrent small-set kernel
 struct AuxStream {
   cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t join = nullptr;
 };
 // keyed by (device, slot): slot 0 serves caller streams, slot k + 1 the k-th
 // internal lane of pmh_sketch_csr_multi_async (so concurrent variants do not
@@ -283,7 +324,6 @@ int get_aux(AuxStream** out, int slot = 0) {
     int least = 0, greatest = 0;
     PMH_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     PMH_CUDA(cudaStreamCreateWithPriority(&a.s, cudaStreamNonBlocking, greatest));
-    PMH_CUDA(cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming));
     PMH_CUDA(cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming));
     it = g_aux.emplace(std::make_pair(dev, slot), a).first;
   }
@@ -348,8 +388,11 @@ cudaError_t launch_pminhash_split(PMinArgs a, int64_t split_n, int64_t split_cap
                        (long long)sms * per_sm, st, &ws)) != cudaSuccess)
     return e;
   a.split_info = ws.sp.info;
-  PMH_CUDA_E(cudaEventRecord(aux->fork, st));
-  PMH_CUDA_E(cudaStreamWaitEvent(aux->s, aux->fork, 0));
+  {
+    ForkEvent fork;
+    PMH_CUDA_E(cudaEventRecord(fork.e, st));
+    PMH_CUDA_E(cudaStreamWaitEvent(aux->s, fork.e, 0));
+  }
   if ((e = launch_pminhash<EXPO>(a, aux->s)) != cudaSuccess) return e;   // remaining sets
   pminhash64_split_kernel<EXPO><<<(unsigned)(sms * per_sm), PMIN_THREADS, smem, st>>>(a, ws.sp);
   split_finalize_kernel<<<(unsigned)(sms * 4), 256, 0, st>>>(ws.sp, a.ids, a.sig);
@@ -363,7 +406,6 @@ cudaError_t launch_pminhash_split(PMinArgs a, int64_t split_n, int64_t split_cap
 struct LanePool {
   std::vector<cudaStream_t> s;
   std::vector<cudaEvent_t> done;
-  cudaEvent_t fork = nullptr;
 };
 std::map<int, LanePool> g_lanes;
 
@@ -372,7 +414,6 @@ int get_lanes(int n, LanePool** out) {
   PMH_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_mu);
   LanePool& p = g_lanes[dev];
-  if (!p.fork) PMH_CUDA(cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming));
   while ((int)p.s.size() < n) {
     cudaStream_t st;
     cudaEvent_t ev;
@@ -414,8 +455,13 @@ int validate_sketch(int algo, int64_t m, const double* weights, int64_t nsets) {
   if (fam != 0 && (sketch_smem_bytes(fam, m, SKETCH_THREADS, sketch_fy16_256(fam, m)) > SMEM_DYN_MAX ||
                    (sketch_fy16_256(fam, m) && m >= 8192)))
     return set_error(PMH_ERR_INVALID, "signature size too large for the shared-memory slot table");
-  if ((algo == ALG_PMINHASH || algo == ALG_MINHASH) && m > 64LL * PMIN_THREADS)
+  // the P-MinHash launchers: the static kernel takes m % 64 == 0 up to
+  // 64 * PMIN_THREADS, the generic one m <= 32 * PMIN_THREADS
+  if ((algo == ALG_PMINHASH || algo == ALG_MINHASH) &&
+      !(m <= 32LL * PMIN_THREADS || (m % PM64_C == 0 && m <= 64LL * PMIN_THREADS)))
     return set_error(PMH_ERR_INVALID, "signature size too large for the P-MinHash kernel");
+  if (algo == ALG_OPH && sizeof(Slot) * (size_t)m > SMEM_DYN_MAX)
+    return set_error(PMH_ERR_INVALID, "signature size too large for the OPH kernel");
   if (m > 65535) return set_error(PMH_ERR_INVALID, "signature size must be <= 65535");
   if (nsets < 0) return set_error(PMH_ERR_INVALID, "negative set count");
   if (nsets > 0 && !is_unweighted(algo) && !weights)
@@ -483,7 +529,8 @@ int pmh_sketch_csr_multi_async(const int* algos, int nalgos, int64_t m, const ui
   LanePool* lp = nullptr;
   int rc = get_lanes(nalgos, &lp);
   if (rc) return rc;
-  PMH_CUDA(cudaEventRecord(lp->fork, st));
+  ForkEvent fork;
+  PMH_CUDA(cudaEventRecord(fork.e, st));
   // the P-MinHash-type variants (one long, tail-light kernel) last: their
   // CTAs fill the tails of the ProbMinHash kernels launched before them
   std::vector<int> order;
@@ -493,7 +540,7 @@ int pmh_sketch_csr_multi_async(const int* algos, int nalgos, int64_t m, const ui
       if (pmin == (pass == 1)) order.push_back(k);
     }
   for (int k : order) {
-    PMH_CUDA(cudaStreamWaitEvent(lp->s[k], lp->fork, 0));
+    PMH_CUDA(cudaStreamWaitEvent(lp->s[k], fork.e, 0));
     rc = sketch_async_impl(algos[k], m, ids, weights, offsets, nsets, sig_outs[k],
                            stats_outs ? stats_outs[k] : nullptr, d_status, lp->s[k], k + 1);
     PMH_CUDA(cudaEventRecord(lp->done[k], lp->s[k]));
@@ -514,6 +561,10 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
   if (!d_status) return set_error(PMH_ERR_INVALID, "status buffer required");
   unsigned long long* flags = reinterpret_cast<unsigned long long*>(d_status);
   long long* d_err_set = reinterpret_cast<long long*>(d_status + 1);
+  {
+    const int crc = apply_test_caps();
+    if (crc != PMH_OK) return crc;
+  }
 
   cudaError_t e;
   if (is_baseline(algo)) {
@@ -594,8 +645,11 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
     AuxStream* aux = nullptr;
     rc = get_aux(&aux, aux_slot);
     if (rc) { cudaFreeAsync(order_ws, st); return rc; }
-    PMH_CUDA(cudaEventRecord(aux->fork, st));
-    PMH_CUDA(cudaStreamWaitEvent(aux->s, aux->fork, 0));
+    {
+      ForkEvent fork;
+      PMH_CUDA(cudaEventRecord(fork.e, st));
+      PMH_CUDA(cudaStreamWaitEvent(aux->s, fork.e, 0));
+    }
     auto big = [&]() {
       switch (fam) {
         case FAM_PMH1: return launch_family<FAM_PMH1>(a, st);
@@ -762,6 +816,8 @@ static int host_multi_impl(const int* algos, int nalgos, int64_t m, const uint64
     any_weighted |= !is_unweighted(algos[k]);
   }
   if (nsets == 0) return PMH_OK;
+  if (!ids || !offsets) return set_error(PMH_ERR_INVALID, "ids and offsets required");
+  if (offsets[0] != 0) return set_error(PMH_ERR_INVALID, "offsets[0] must be 0");
   if (offsets[nsets] != nelems) return set_error(PMH_ERR_INVALID, "offsets[nsets] != nelems");
   for (int64_t s = 0; s < nsets; s++)  // host buffers: report empties up front
     if (offsets[s + 1] <= offsets[s]) {
@@ -1216,7 +1272,8 @@ int64_t pmh_parse_weighted_text(const char* buf, int64_t len, uint64_t* ids, dou
   return pmh_ingest::parse_weighted_text(buf, len, ids, weights, cap);
 }
 
-int pmh_probe_alu_peak(double* gops_out, double* ms_out) {
+int pmh_probe_pipe_peak(int kind, double* gops_out, double* ms_out) {
+  if (kind < PROBE_LOP3 || kind > PROBE_FFMA) return set_error(PMH_ERR_INVALID, "unknown probe");
   int dev = 0, sms = 0;
   PMH_CUDA(cudaGetDevice(&dev));
   PMH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1225,25 +1282,85 @@ int pmh_probe_alu_peak(double* gops_out, double* ms_out) {
   cudaEvent_t a, b;
   PMH_CUDA(cudaEventCreate(&a));
   PMH_CUDA(cudaEventCreate(&b));
-  const int blocks = sms * 8, threads = 256, iters = 16384;
-  alu_probe_kernel<<<blocks, threads>>>(256, d);  // warm-up
+  // 8 CTAs x 256 threads per SM = full occupancy at <= 32 registers
+  const int blocks = sms * 8, threads = 256;
+  const int iters = kind == PROBE_DFMA ? 4096 : 16384;
+  auto launch = [&](int it) {
+    switch (kind) {
+      case PROBE_LOP3: alu_probe_kernel<<<blocks, threads>>>(it, d); break;
+      case PROBE_IMAD: imad_probe_kernel<<<blocks, threads>>>(it, d); break;
+      case PROBE_DFMA: dfma_probe_kernel<<<blocks, threads>>>(it, d); break;
+      default: ffma_probe_kernel<<<blocks, threads>>>(it, d); break;
+    }
+  };
+  launch(256);  // warm-up
   float ms = 1e30f;
   for (int rep = 0; rep < 5; rep++) {  // best of 5 (clock ramp / co-tenant noise)
     PMH_CUDA(cudaEventRecord(a));
-    alu_probe_kernel<<<blocks, threads>>>(iters, d);
+    launch(iters);
     PMH_CUDA(cudaEventRecord(b));
     PMH_CUDA(cudaEventSynchronize(b));
     float t = 0.f;
     PMH_CUDA(cudaEventElapsedTime(&t, a, b));
     ms = t < ms ? t : ms;
   }
+  PMH_CUDA(cudaGetLastError());
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(d);
-  const double ops = (double)blocks * threads * iters * 16.0 * 8.0;
+  const double ops = (double)blocks * threads * iters * 16.0 * 8.0;   // thread-level ops
   if (gops_out) *gops_out = ops / (ms * 1e-3) / 1e9;
   if (ms_out) *ms_out = ms;
   return PMH_OK;
+}
+
+int pmh_math_eval(int fn, const double* x, int64_t n, double* out, void* stream) {
+  if (fn < 0 || fn > 1 || n < 0) return set_error(PMH_ERR_INVALID, "fn must be 0 (log1p) or 1 (expm1)");
+  if (n == 0) return PMH_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  math_eval_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(fn, x, n, out);
+  PMH_CUDA(cudaGetLastError());
+  return PMH_OK;
+}
+
+int pmh_probe_point_rate(int kind, double* gpts_out, double* ms_out) {
+  if (kind < 0 || kind > 1) return set_error(PMH_ERR_INVALID, "kind must be 0 (log1p) or 1 (TruncExp)");
+  int dev = 0, sms = 0;
+  PMH_CUDA(cudaGetDevice(&dev));
+  PMH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  uint32_t* d = nullptr;
+  PMH_CUDA(cudaMalloc(&d, 16));
+  cudaEvent_t a, b;
+  PMH_CUDA(cudaEventCreate(&a));
+  PMH_CUDA(cudaEventCreate(&b));
+  int per_sm = 1;
+  auto kern = kind == 0 ? point_probe_kernel<0> : point_probe_kernel<1>;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+  const int blocks = sms * (per_sm > 0 ? per_sm : 1), threads = 256;
+  const int iters = kind == 0 ? 2048 : 8192;
+  kern<<<blocks, threads>>>(64, d);   // warm-up
+  float ms = 1e30f;
+  for (int rep = 0; rep < 5; rep++) {
+    PMH_CUDA(cudaEventRecord(a));
+    kern<<<blocks, threads>>>(iters, d);
+    PMH_CUDA(cudaEventRecord(b));
+    PMH_CUDA(cudaEventSynchronize(b));
+    float t = 0.f;
+    PMH_CUDA(cudaEventElapsedTime(&t, a, b));
+    ms = t < ms ? t : ms;
+  }
+  PMH_CUDA(cudaGetLastError());
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(d);
+  if (gpts_out) *gpts_out = (double)blocks * threads * iters / (ms * 1e-3) / 1e9;
+  if (ms_out) *ms_out = ms;
+  return PMH_OK;
+}
+
+int pmh_probe_alu_peak(double* gops_out, double* ms_out) {
+  return pmh_probe_pipe_peak(PROBE_LOP3, gops_out, ms_out);
 }
 
 }  // extern "C"

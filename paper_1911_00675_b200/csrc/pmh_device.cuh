@@ -36,6 +36,14 @@ constexpr double INV53 = 1.1102230246251565e-16;    // K:30
 constexpr uint64_t OPH_SALT = 0xA24BAED4963EE407ULL;  // K:33
 constexpr int REJECT_CAP = 4096;                    // K:37
 
+// The loop caps the device code enforces: the reference's REJECT_CAP (K:37)
+// and coupon cap (K:279-281).  Always these values, except that a TEST may
+// lower them through the environment (PMH_TEST_REJECT_CAP /
+// PMH_TEST_COUPON_CAP, read once per device by the host, pmh_capi.cu) to
+// drive the RandomnessFailureError path on the device.
+__constant__ int g_reject_cap = REJECT_CAP;
+__constant__ long long g_coupon_cap_override = 0;   // > 0: replaces the K:279-281 cap
+
 // algorithm ids = K:866-881
 enum Algo : int {
   ALG_PMINHASH = 0, ALG_PMH1 = 1, ALG_PMH1A = 2, ALG_PMH2 = 3, ALG_PMH3 = 4,
@@ -125,7 +133,7 @@ __device__ __forceinline__ int64_t uniform_int_masked(Stream& st, uint64_t n,
   for (int rounds = 0;; ) {
     uint64_t r = st.next_bits(kbits);
     if (r < n) return (int64_t)r;
-    if (++rounds > REJECT_CAP) return -1;
+    if (++rounds > g_reject_cap) return -1;
   }
 }
 __device__ __forceinline__ int64_t uniform_int(Stream& st, int64_t n) {  // K:113-117
@@ -163,7 +171,7 @@ __device__ __noinline__ double trunc_exp_slow(Stream& st, const TruncExpConsts& 
     double e = g_expm1(c.lam * (1.0 - x), &ok);
     if (!ok) { *fail = true; return 0.0; }
     if (y * c.c1 * c.lam <= e) return x;
-    if (++rounds > REJECT_CAP) { *fail = true; return 0.0; }
+    if (++rounds > g_reject_cap) { *fail = true; return 0.0; }
   }
 }
 __device__ __forceinline__ double trunc_exp(Stream& st, const TruncExpConsts& c,

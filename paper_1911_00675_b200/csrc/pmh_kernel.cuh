@@ -51,6 +51,12 @@ __device__ __forceinline__ bool first_point_rejects(const Tables& T, uint64_t id
     return t * lo > thr * w * hi && 1.0 * lo > thr * w * hi;
   }
 }
+// K:279-281 (or a test's lowered cap, pmh_device.cuh)
+__device__ __forceinline__ int64_t coupon_cap(int64_t m) {
+  if (g_coupon_cap_override > 0) return (int64_t)g_coupon_cap_override;
+  return (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
+}
+
 constexpr int SKETCH_THREADS = 256;
 // dynamic shared memory per CTA: the 227 KB opt-in limit counts the kernels'
 // static __shared__ state too (SetShared and friends, < 1 KB)
@@ -286,7 +292,7 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
   c.filled = &sh.filled;
   c.m = m;
   c.kbits = bits_for(m);
-  c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
+  c.cap = coupon_cap(m);
   c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
   c.trig = false;
   c.eoff = e0;
@@ -531,7 +537,7 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
     c.filled = &wv->filled;
     c.m = m;
     c.kbits = bits_for(m);
-    c.cap = (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
+    c.cap = coupon_cap(m);
     c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
   c.trig = false;
     c.eoff = 0;

@@ -258,7 +258,7 @@ __device__ void parse_fy_cursor(const SetCtx& c, WarpScratch& ws, uint64_t id, u
         const uint64_t v = win_bits(ws.words, c2, kb);
         c2 += kb;
         if (v < (uint64_t)R) { r = (int64_t)v; break; }
-        if (++rounds > REJECT_CAP) { flags = 2u; break; }
+        if (++rounds > g_reject_cap) { flags = 2u; break; }
       }
       if (flags) break;
       if (!fits) {

@@ -112,6 +112,7 @@ class AllPairsResult:
     hist: np.ndarray          # int64[m+1]: number of pairs (i<j) with count c
     pairs: np.ndarray         # int64[K, 3]: (i, j, count) with count >= threshold
     tiles: int
+    total: int = -1           # pairs with count >= threshold found (== len(pairs))
 
 
 def allpairs_local(sigs_all, rows, tile, threshold, count_tile_fn):
@@ -139,7 +140,7 @@ def allpairs_local(sigs_all, rows, tile, threshold, count_tile_fn):
                 found.append(np.stack([iw + r0, jw + c0, cnt[sel]], axis=1).astype(np.int64))
             tiles += 1
     pairs = np.concatenate(found) if found else np.zeros((0, 3), np.int64)
-    return AllPairsResult(hist, pairs, tiles)
+    return AllPairsResult(hist, pairs, tiles, len(pairs))
 
 
 def _gpu_count_tile(sigs_all, r0, r1, c0, c1):
@@ -148,29 +149,56 @@ def _gpu_count_tile(sigs_all, r0, r1, c0, c1):
     return out.cpu().numpy().view(np.uint16)
 
 
-def _gpu_rows_hist(sigs_all, rows, tile, threshold):
-    """This rank's block rows on the GPU with the fused histogram kernel."""
+def _gpu_rows_hist(sigs_all, rows, tile, threshold, cap=1 << 22):
+    """This rank's block rows on the GPU with the fused histogram kernel.
+
+    The kernel lists at most `cap` pairs per call but always returns the
+    exact total k; a block row whose k exceeds the cap is recomputed with
+    cap = k (into a fresh histogram, so nothing is counted twice), so the
+    pair list is never truncated."""
     import torch
     from .batch import allpairs_hist_device
     n, m = sigs_all.shape
     hist = torch.zeros(m + 1, dtype=torch.int64, device=sigs_all.device)
     found = []
+    total = 0
     for b in rows:
         r0, r1 = b * tile, min(n, (b + 1) * tile)
-        _, pairs, k = allpairs_hist_device(sigs_all, r0, r1, r0, n, threshold, hist=hist)
+        h_b = torch.zeros(m + 1, dtype=torch.int64, device=sigs_all.device)
+        _, pairs, k = allpairs_hist_device(sigs_all, r0, r1, r0, n, threshold, cap=cap, hist=h_b)
+        if k > cap:
+            h_b.zero_()
+            _, pairs, k2 = allpairs_hist_device(sigs_all, r0, r1, r0, n, threshold, cap=k,
+                                                hist=h_b)
+            if k2 != k or len(pairs) != k:
+                raise RuntimeError(f"all-pairs block row {b}: pair list {len(pairs)} != {k}")
+        hist += h_b
+        total += k
         found.append(pairs)
     pairs = np.concatenate(found) if found else np.zeros((0, 3), np.int64)
-    return AllPairsResult(hist.cpu().numpy(), pairs, len(rows))
+    return AllPairsResult(hist.cpu().numpy(), pairs, len(rows), total)
+
+
+def _stamp(dev):
+    import time
+    if dev.type == "cuda":
+        import torch
+        torch.cuda.synchronize(dev)
+    return time.perf_counter()
 
 
 def allpairs_distributed(local_sigs, rank, world, tile=4096, threshold=1, group=None,
-                         count_tile_fn=None):
+                         count_tile_fn=None, cap=1 << 22, ms=None):
     """All-gather the sharded signatures, compute this rank's block rows and
     all_reduce the histogram.  local_sigs: torch tensor [n_r, m] (int64, on
     the rank's device for NCCL; CPU for gloo).  Ranks may hold different row
-    counts (padded for the all_gather)."""
+    counts (padded for the all_gather).  `ms` (a dict), if given, receives
+    this rank's device-synchronised milliseconds of the all-gather, the
+    block-row compute and the histogram all_reduce."""
     import torch
     import torch.distributed as dist
+    dev = local_sigs.device
+    t0 = _stamp(dev)
     n_r = torch.tensor([local_sigs.shape[0]], device=local_sigs.device, dtype=torch.int64)
     sizes = [torch.zeros_like(n_r) for _ in range(world)]
     dist.all_gather(sizes, n_r, group=group)
@@ -182,13 +210,19 @@ def allpairs_distributed(local_sigs, rank, world, tile=4096, threshold=1, group=
     gathered = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(gathered, pad, group=group)
     sigs_all = torch.cat([g[:s] for g, s in zip(gathered, sizes)], dim=0)
+    t1 = _stamp(dev)
     n = sigs_all.shape[0]
     rows = block_rows(n, tile, world)[rank]
     if count_tile_fn is None:
-        res = _gpu_rows_hist(sigs_all, rows, tile, threshold)
+        res = _gpu_rows_hist(sigs_all, rows, tile, threshold, cap)
     else:
         res = allpairs_local(sigs_all, rows, tile, threshold, count_tile_fn)
+    t2 = _stamp(dev)
     h = torch.from_numpy(res.hist).to(local_sigs.device)
     dist.all_reduce(h, group=group)
     res.hist = h.cpu().numpy()
+    t3 = _stamp(dev)
+    if ms is not None:
+        ms.update({"allgather": (t1 - t0) * 1e3, "block_rows": (t2 - t1) * 1e3,
+                   "hist_allreduce": (t3 - t2) * 1e3})
     return res

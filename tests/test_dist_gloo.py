@@ -14,6 +14,7 @@ import torch.multiprocessing as mp
 from oracle import oracle as orc
 from paper_1911_00675_b200 import datagen
 from paper_1911_00675_b200 import dist as pdist
+from paper_1911_00675_b200 import similarity as psim
 
 
 def _free_port():
@@ -117,3 +118,64 @@ def test_gloo_world2_sharded_sketch_and_allpairs():
     pairs = np.concatenate([o[4] for o in out])
     exp_pairs = {(int(i), int(j), int(full[i, j])) for i, j in zip(*iu) if full[i, j] >= 1}
     assert {tuple(map(int, p)) for p in pairs} == exp_pairs
+
+
+def _pairs_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        b, jt, jx = datagen.config5_pairs(npairs=45, n=40, seed=9)
+        res = psim.run_pairs(b, jt, jx, 16, rank, world, tile=8, sketch_fn=_oracle_sketch,
+                             count_tile_fn=_oracle_tile)
+        q.put((rank, res.summary(), res.hist.copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_pairs_pipeline_matches_single_process():
+    """configs[4] pipeline (similarity.run_pairs): sharded sketch, all-gather,
+    block rows, designed-pair statistics reduced over 2 ranks == one process."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_pairs_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=180) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    b, jt, jx = datagen.config5_pairs(npairs=45, n=40, seed=9)
+    m = 16
+    ref, _ = orc.sketch_csr("probminhash4", m, b.ids, b.weights, b.offsets)
+    cnt = orc.count_equal(ref[0::2], ref[1::2])
+    stats = psim.bucket_stats(psim.bucket_sums(jt, jx, cnt, m), m)
+    full = orc.allpairs(ref)
+    iu = np.triu_indices(ref.shape[0], 1)
+    exp_hist = np.bincount(full[iu], minlength=m + 1)
+    designed = {(2 * p, 2 * p + 1) for p in range(45)}
+    extra = sum(1 for i, j in zip(*iu) if full[i, j] >= 1 and (i, j) not in designed)
+    for rank, summ, hist in out:
+        np.testing.assert_array_equal(hist, exp_hist)
+        assert summ["extra_pairs"] == extra
+        assert [bk["pairs"] for bk in summ["buckets"]] == [s.pairs for s in stats]
+        for bk, s in zip(summ["buckets"], stats):
+            assert bk["mean_err"] == pytest.approx(s.mean_err, abs=1e-12)
+            assert bk["mse"] == pytest.approx(s.mse, rel=1e-12, abs=1e-15)
+
+
+def test_bucket_stats_and_designed_counts():
+    jt = np.array([0.1, 0.1, 0.5, 0.5, 0.5])
+    jx = np.array([0.1, 0.12, 0.5, 0.49, 0.51])
+    pairs = np.array([[0, 1, 2], [2, 3, 1], [4, 5, 8], [6, 7, 7], [8, 9, 9], [1, 4, 1]])
+    counts, extra = psim.designed_counts(pairs, 0, 5)
+    assert counts.tolist() == [2, 1, 8, 7, 9] and extra == 1
+    st = psim.bucket_stats(psim.bucket_sums(jt, jx, counts, 16), 16)
+    assert [s.pairs for s in st] == [2, 3]
+    err = counts / 16 - jx
+    assert st[0].mean_err == pytest.approx(err[:2].mean())
+    assert st[1].mse == pytest.approx((err[2:] ** 2).mean())
+    assert st[1].z_mean == pytest.approx(err[2:].mean() / (err[2:].std(ddof=1) / np.sqrt(3)))
+    assert psim.two_sample_mse_z([0.1, -0.1, 0.2], [0.1, -0.1, 0.2]) == 0.0
