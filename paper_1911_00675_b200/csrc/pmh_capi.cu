@@ -428,6 +428,16 @@ int get_lanes(int n, LanePool** out) {
 
 template <int F>
 cudaError_t launch_small(const SketchArgs& a, cudaStream_t st) {
+  if (wps_eligible(F, a.m)) {   // small m: the lean warp-per-set kernel (pmh_wps.cuh)
+    const size_t smem = sizeof(WpsWarp) * (WPS_THREADS / 32);
+    cudaError_t e = cudaFuncSetAttribute(sketch_wps_kernel<F>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int64_t grid = (a.nsets + (WPS_THREADS / 32) - 1) / (WPS_THREADS / 32);
+    if (grid > 148 * 32) grid = 148 * 32;
+    sketch_wps_kernel<F><<<(unsigned)grid, WPS_THREADS, smem, st>>>(a);
+    return cudaGetLastError();
+  }
   const size_t per_warp = small_warp_bytes(F, a.m);
   int wpc = (int)((96 * 1024) / per_warp);
   wpc = wpc < 1 ? 1 : (wpc > 4 ? 4 : wpc);

@@ -181,6 +181,19 @@ __device__ __forceinline__ double trunc_exp(Stream& st, const TruncExpConsts& c,
   return trunc_exp_slow(st, c, fail);
 }
 
+// Asynchronous 8-byte global -> shared copies (cp.async): element chunks and
+// sets stream into shared memory while the warp works on the previous ones.
+// 8-byte granularity because set offsets are arbitrary.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_group1() {
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------
 // Slot table: per component k the lexicographic minimum of (h, element index)
 // over all generated points -- the exact semantics of the reference's strict

@@ -25,6 +25,7 @@ namespace pmh {
 #endif
 constexpr double HEAVY_POINTS = PMH_HEAVY_POINTS;   // expected points above which mode B runs
 
+
 // Division-free prefilter for the common case of large sets: decide from the
 // element's first stream word whether its FIRST point exceeds thr and the
 // SECOND point's lower bound does too, in which case the element contributes
@@ -56,6 +57,11 @@ __device__ __forceinline__ int64_t coupon_cap(int64_t m) {
   if (g_coupon_cap_override > 0) return (int64_t)g_coupon_cap_override;
   return (int64_t)(64.0 * (double)m * (1.0 + log((double)m)) + 64.0);
 }
+
+
+}  // namespace pmh
+#include "pmh_wps.cuh"
+namespace pmh {
 
 constexpr int SKETCH_THREADS = 256;
 // dynamic shared memory per CTA: the 227 KB opt-in limit counts the kernels'
@@ -476,6 +482,7 @@ constexpr int64_t SMALL_N_STATIC = PMH_SMALL_N_STATIC;
 // warp-per-set cutoff: for m <= 256 whole sets of up to 512 elements are cheap
 // enough for one warp (configs[3], configs[4]); for large m only tiny sets
 __host__ __device__ inline int64_t small_n_for(int family, int64_t m) {
+  if (wps_eligible(family, m)) return (int64_t)WPS_NMAX;   // pmh_wps.cuh
   if (m <= 256) return (int64_t)PMH_SMALL_N_SMALLM;
   return family_uses_fy(family) ? SMALL_N : SMALL_N_STATIC;
 }

@@ -43,8 +43,8 @@ struct WarpScratch {
   uint64_t next_off;    // absolute bit offset after the batch
   uint32_t epoch;       // Fisher-Yates map epoch (one per warp-processed element)
   uint32_t pad;
-  int32_t sq[SQ_CAP];   // survivor queue of the large-set path (element indices, LIFO)
   uint32_t gm[32];      // parallel Fisher-Yates: lanes whose target is i0 + k
+  int32_t sq[SQ_CAP];   // survivor queue of the large-set path (element indices, LIFO)
 };
 
 // Dense per-warp Fisher-Yates map with O(1) reset: entry = epoch << 16 | value
@@ -186,6 +186,152 @@ __device__ int warp_el_static(SetCtx& c, const Tables& T, WarpScratch& ws, int l
     } else {  // PMH3: speculate on TruncExp's fast path
       double t = T.c3.c1 * ((double)u * INV53);
       const unsigned slow = __ballot_sync(0xffffffffu, in && !(t < 1.0));
+      if (slow) {
+        const int f = __ffs(slow) - 1;
+        ncand = (uint32_t)f + 1;
+        had_slow = true;
+        if (lane == f) {
+          Stream st;
+          st.seek(id, off + (uint64_t)f * P + 53);
+          bool fail = false;
+          t = trunc_exp_slow(st, T.c3, &fail);
+          lab = (int32_t)st.next_bits(kb) + 1;
+          ws.next_off = st.pos(id);
+          ws.flags = fail ? 2u : 0u;
+        }
+        __syncwarp();
+        if (ws.flags & 2u) return EL_FAIL;
+      }
+      xv = pt == 1 ? winv * t : winv * ((double)pt - 1.0) + winv * t;
+    }
+    const bool cand = (uint32_t)lane < ncand;
+    const bool valid = cand && xv <= thr;
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    const bool trig = valid ? offer_trig(c, lab - 1, xv, e) : false;
+    if (__any_sync(0xffffffffu, trig)) hmax_refresh_warp(c, lane);
+    const uint32_t nv = __popc(vm);
+    // a retry attempt only counts points above the previous threshold
+    const uint32_t nn = __popc(__ballot_sync(0xffffffffu, cand && !(xv <= c.tprev)));
+    if (lane == 0) c.points += (c.tprev < 0.0 ? nv + (nv < ncand ? 1 : 0) : nn);
+    if (nv < ncand) return EL_DONE;
+    i += ncand;
+    if (i > c.cap) return EL_FAIL;
+    if constexpr (F == FAM_PMH1) x = __shfl_sync(0xffffffffu, xv, ncand - 1);
+    if (had_slow) off = ws.next_off;
+    else off += (uint64_t)ncand * P;
+    __syncwarp();
+  }
+}
+
+// Exact warp-parallel version of the ordered fold x_j = fl(x_{j-1} + d_j)
+// (K:328, K:440): lane j returns x_j, x_{-1} = x0.  While the running sum
+// stays in one binade [2^e, 2^(e+1)) every rounding is onto the same grid
+// u = 2^(e-52), so with x_{j-1} on the grid
+//     fl(x_{j-1} + d_j) = x_{j-1} + u * rint(d_j / u)
+// except on an exact tie (d_j / u = k + 1/2, where IEEE rounds to the EVEN
+// result, which depends on x_{j-1}).  The grid increments g_j = u rint(d_j/u)
+// are multiples of u, so their prefix sums below 2^(e+1) are exact in
+// floating point in any association: a Kogge-Stone scan reproduces the
+// sequential chain bit for bit.  Lanes from the first tie or binade exit on
+// are redone from the last exact value (one sequential add, then a new scan
+// on the new binade); a batch normally needs one scan, rarely two.  x0 == 0
+// (the element's first point): fl(0 + d_0) = d_0.
+__device__ __forceinline__ double grid_fold(double x0, double d, int lane) {
+  double base = x0;
+  int start = 0;
+  double res = 0.0;
+  if (x0 == 0.0) {
+    base = __shfl_sync(0xffffffffu, d, 0);
+    res = base;
+    start = 1;
+  }
+  while (start < 32) {
+    const uint64_t bb = dbl_bits(base);
+    const uint64_t ex = bb >> 52;            // base >= 0: the biased exponent
+    if (ex < 53 || ex > 2044) {
+      // zero / tiny / huge running sum (never seen in practice): sequential
+      double acc = base;
+      for (int j = start; j < 32; j++) {
+        acc = acc + __shfl_sync(0xffffffffu, d, j);
+        if (lane == j) res = acc;
+      }
+      return res;
+    }
+    const double inv_u = bits_dbl((2098ULL - ex) << 52);   // 2^(52 - e)
+    const double u = bits_dbl((ex - 52ULL) << 52);          // 2^(e - 52)
+    const double lim = bits_dbl((ex + 1ULL) << 52);         // 2^(e + 1)
+    const bool mine = lane >= start;
+    const double k = mine ? d * inv_u : 0.0;
+    const double r = rint(k);
+    const double fr = k - r;
+    const bool tie = mine && (fr == 0.5 || fr == -0.5);
+    double S = r * u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, S, o);
+      if (lane >= o) S = S + t;
+    }
+    const double cand = base + S;
+    const bool bad = mine && (tie || !(cand < lim));
+    const unsigned bm = __ballot_sync(0xffffffffu, bad);
+    const int f = bm ? __ffs(bm) - 1 : 32;
+    if (mine && lane < f) res = cand;
+    if (f == 32) break;
+    const double prev = f == start ? base : __shfl_sync(0xffffffffu, cand, f - 1);
+    const double xf = prev + __shfl_sync(0xffffffffu, d, f);   // the sequential step
+    if (lane == f) res = xf;
+    base = xf;
+    start = f + 1;
+  }
+  return res;
+}
+
+#ifndef PMH_GRIDFOLD_FROM
+#define PMH_GRIDFOLD_FROM 64   // grid_fold for batches starting beyond this point index
+#endif
+
+// Mode B for labels with replacement at label widths kb <= 11 (points of
+// 53 + kb <= 64 bits): a window of 33 stream words always holds 32 whole
+// points, each lane's point lies in two adjacent words (one funnel shift
+// gives its 53 value bits and its label), and ProbMinHash1's running sum
+// folds with grid_fold.  Same results and counters as warp_el_static.
+template <int F>
+__device__ int warp_el_static2(SetCtx& c, const Tables& T, WarpScratch& ws, int lane,
+                               int64_t e, uint64_t id, double winv) {
+  const uint32_t kb = c.kbits;
+  const uint32_t P = 53 + kb;
+  const uint64_t kmask = (1ULL << kb) - 1ULL;
+  uint64_t off = 0;     // absolute bit offset of the next point
+  int64_t i = 1;        // next point index (1-based)
+  double x = 0.0;       // PMH1 running sum
+  for (;;) {
+    const uint64_t wb = off >> 6;
+    ws.words[lane] = stream_word(id, wb + 1 + (uint64_t)lane);
+    if (lane == 0) ws.words[32] = stream_word(id, wb + 33);
+    __syncwarp();
+    const uint32_t rel0 = (uint32_t)(off & 63);
+    const double thr = warp_thr(c);
+    const int64_t pt = i + lane;
+    const uint32_t ro = rel0 + (uint32_t)lane * P;
+    const uint32_t wi = ro >> 6, sh = ro & 63;
+    const uint64_t w0 = ws.words[wi];
+    const uint64_t v = sh ? (w0 >> sh) | (ws.words[wi + 1] << (64 - sh)) : w0;
+    const uint64_t u = v & ((1ULL << 53) - 1ULL);
+    int32_t lab = (int32_t)((v >> 53) & kmask) + 1;
+    double xv = 0.0;
+    uint32_t ncand = 32;
+    bool had_slow = false;
+    if constexpr (F == FAM_PMH1) {
+      // the first batches cross binades at almost every doubling of x
+      // (many grid_fold rounds): the sequential fold there
+      const double d = winv * exp1_from_bits(u);
+      xv = i <= PMH_GRIDFOLD_FROM ? ordered_fold(ws, x, d, lane, 32) : grid_fold(x, d, lane);
+    } else if constexpr (F == FAM_UW3) {
+      const double U = (double)u * INV53;
+      xv = pt == 1 ? U : ((double)pt - 1.0) + U;
+    } else {  // PMH3: speculate on TruncExp's fast path
+      double t = T.c3.c1 * ((double)u * INV53);
+      const unsigned slow = __ballot_sync(0xffffffffu, !(t < 1.0));
       if (slow) {
         const int f = __ffs(slow) - 1;
         ncand = (uint32_t)f + 1;
@@ -572,8 +718,13 @@ template <int F, bool FY16>
 __device__ __forceinline__ int warp_element(SetCtx& c, const Tables& T, WarpScratch& ws,
                                             uint32_t* fy, int lane, int64_t e, uint64_t id,
                                             double winv) {
-  if constexpr (F == FAM_PMH1 || F == FAM_PMH3 || F == FAM_UW3)
+  if constexpr (F == FAM_PMH1 || F == FAM_PMH3 || F == FAM_UW3) {
+#ifndef PMH_STATIC2
+#define PMH_STATIC2 1
+#endif
+    if (PMH_STATIC2 && c.kbits <= 11) return warp_el_static2<F>(c, T, ws, lane, e, id, winv);
     return warp_el_static<F>(c, T, ws, lane, e, id, winv);
+  }
   else
     return warp_el_fy<F, FY16>(c, T, ws, fy, lane, e, id, winv);
 }
