@@ -315,7 +315,7 @@ class Step:
     """One configs[1] batch resident on this rank's GPU and its step launcher
     (every variant through the asynchronous C ABI entry, no host sync)."""
 
-    def __init__(self, ctx, batch, variants, concurrent=False):
+    def __init__(self, ctx, batch, variants, concurrent=False, shared_w=True):
         torch = ctx.torch
         from paper_1911_00675_b200 import _lib
         from paper_1911_00675_b200.batch import to_device_f64, to_device_i64, to_device_u64
@@ -335,11 +335,30 @@ class Step:
         self.arr_a = (ctypes.c_int * len(variants))(*[_lib.ALG[v] for v in variants])
         self.arr_s = (ctypes.c_void_p * len(variants))(*[t.data_ptr() for t in self.sigs_multi])
         self.ev = {v: [] for v in variants}
+        # the sets' total weights, computed ONCE per step for all variants
+        # (pmh_set_weights; each kernel would otherwise re-read every weight
+        # for its threshold guess) -- inside the timed step
+        self.shared_w = shared_w
+        self.setw = torch.empty(self.S, dtype=torch.float64, device="cuda")
+        self.ev["set_weights"] = []
+
+    def launch_setw(self, timed=False):
+        if timed:
+            torch = self.ctx.torch
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(self.stream)
+        self.lib.check(self.L.pmh_set_weights(self.w.data_ptr(), self.off.data_ptr(), self.S,
+                                              self.setw.data_ptr(), self.sp))
+        if timed:
+            b.record(self.stream)
+            self.ev["set_weights"].append((a, b))
 
     def launch(self, v):
-        self.lib.check(self.L.pmh_sketch_csr_async(
+        self.lib.check(self.L.pmh_sketch_csr_w_async(
             self.lib.ALG[v], M, self.ids.data_ptr(), self.w.data_ptr(), self.off.data_ptr(),
-            self.S, self.sig.data_ptr(), None, self.status.data_ptr(), self.sp))
+            self.S, self.setw.data_ptr() if self.shared_w else None, self.sig.data_ptr(), None,
+            self.status.data_ptr(), self.sp))
 
     def timed_launch(self, v):
         torch = self.ctx.torch
@@ -356,6 +375,8 @@ class Step:
                 self.arr_a, len(self.variants), M, self.ids.data_ptr(), self.w.data_ptr(),
                 self.off.data_ptr(), self.S, self.arr_s, None, self.status.data_ptr(), self.sp))
             return
+        if self.shared_w:
+            self.launch_setw(timed)
         for v in self.variants:
             self.timed_launch(v) if timed else self.launch(v)
 
@@ -393,6 +414,10 @@ class Step:
             torch.cuda.synchronize()
         return {v: float(np.mean([a.elapsed_time(b) for a, b in self.ev[v]])) if self.ev[v]
                 else None for v in self.variants}
+
+    def setw_ms(self):
+        e = self.ev["set_weights"]
+        return float(np.mean([a.elapsed_time(b) for a, b in e])) if e else 0.0
 
 
 def run_e2e(ctx, step, steps):
@@ -471,7 +496,7 @@ def run_config2(args, ctx):
     else:
         full = None
         batch = datagen.config2(seed=2 + rank)
-    step = Step(ctx, batch, variants, args.concurrent)
+    step = Step(ctx, batch, variants, args.concurrent, shared_w=not args.no_shared_w)
     clk = ClockSampler(ctx.local)
     ms_step = step.run(args.steps, args.warmup, clk)
     per_variant_ms = step.per_variant_ms(args.per_variant_reps)
@@ -481,7 +506,7 @@ def run_config2(args, ctx):
     weak = None
     if world > 1 and args.scaling == "strong" and not args.no_weak:
         wb = datagen.config2(seed=2 + rank)
-        wstep = Step(ctx, wb, variants, args.concurrent)
+        wstep = Step(ctx, wb, variants, args.concurrent, shared_w=not args.no_shared_w)
         wms = wstep.run(args.steps, args.warmup)
         wn = ctx.reduce(wb.nelems, "sum")
         weak = {"value": len(variants) * wn / (wms / 1e3), "ms_per_step": wms,
@@ -556,7 +581,8 @@ def run_config2(args, ctx):
     # per variant call: 3 ordering kernels; P-MinHash: + split prep, table
     # init, split kernel, finalize, the regular kernel (8); ProbMinHash
     # families: + the small-set kernel (9)
-    launches = args.steps * sum(8 if v == "pminhash" else 9 for v in variants)
+    launches = args.steps * (sum(8 if v == "pminhash" else 9 for v in variants)
+                             + (0 if args.no_shared_w else 1))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -570,6 +596,7 @@ def run_config2(args, ctx):
                    "schedule": ("concurrent (pmh_sketch_csr_multi_async)" if args.concurrent
                                 else "sequential, per-launch CUDA events in the timed region")},
         "per_variant_ms": per_variant_ms,
+        "set_weights_ms": step.setw_ms(),
         "per_variant": per_variant,
         "e2e": e2e,
         "gpu_launches": launches,
@@ -630,6 +657,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-weak", action="store_true")
+    ap.add_argument("--no-shared-w", action="store_true",
+                    help="every variant sums the set weights itself (no pmh_set_weights pass)")
     ap.add_argument("--per-variant-reps", type=int, default=2,
                     help="untimed passes that time each variant alone (--concurrent only)")
     ap.add_argument("--concurrent", action="store_true",

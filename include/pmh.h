@@ -104,6 +104,26 @@ int pmh_sketch_csr_multi_async(const int* algos, int nalgos, int64_t m, const ui
                                const double* weights, const int64_t* offsets, int64_t nsets,
                                uint64_t* const* sig_outs, int64_t* const* stats_outs,
                                int64_t* d_status, void* stream);
+/*
+ * The asynchronous sketch with the sets' total weights KNOWN IN ADVANCE:
+ * set_weights is a DEVICE float64[nsets] (W_s = sum of set s's weights), or
+ * NULL to compute them.  This is the non-streaming form of ProbMinHash2/4
+ * (BASELINE configs[3]; the reference has no non-streaming code): the kernels
+ * skip their weight pre-pass and size the threshold guess from W_s.  Any
+ * positive W_s gives the SAME signature (the final verification max_k h_k <=
+ * guess makes every guess exact-safe; a wrong W_s only costs time).  Accepted
+ * for every weighted algorithm; ignored by the unweighted ones.
+ */
+int pmh_sketch_csr_w_async(int algo, int64_t m, const uint64_t* ids, const double* weights,
+                           const int64_t* offsets, int64_t nsets, const double* set_weights,
+                           uint64_t* sig_out, int64_t* stats_out, int64_t* d_status,
+                           void* stream);
+
+/* Per-set total weights of a CSR batch (DEVICE buffers, stream-ordered):
+ * out[s] = sum of weights[offsets[s] .. offsets[s+1]). */
+int pmh_set_weights(const double* weights, const int64_t* offsets, int64_t nsets, double* out,
+                    void* stream);
+
 int pmh_status_reset(int64_t* d_status, void* stream);
 int pmh_status_check(const int64_t* d_status, int64_t* err_set, void* stream);
 

@@ -40,7 +40,8 @@ EXPORTS = ("pmh_version", "pmh_last_error", "pmh_sketch_csr", "pmh_sketch_csr_as
            "pmh_count_equal", "pmh_allpairs_tile", "pmh_allpairs_hist", "pmh_bbit",
            "pmh_bbit_words", "pmh_bbit_pack", "pmh_allpairs_bbit_hist",
            "pmh_mse_cell", "pmh_parse_weighted_text", "pmh_probe_alu_peak",
-           "pmh_probe_pipe_peak", "pmh_probe_point_rate", "pmh_math_eval")
+           "pmh_probe_pipe_peak", "pmh_probe_point_rate", "pmh_math_eval",
+           "pmh_sketch_csr_w_async", "pmh_set_weights")
 
 _lib = None
 _lock = threading.Lock()
@@ -120,6 +121,11 @@ def load():
         L.pmh_probe_point_rate.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(ctypes.c_double)]
         L.pmh_probe_point_rate.restype = ctypes.c_int
+        L.pmh_sketch_csr_w_async.argtypes = [ctypes.c_int, _i64, _vp, _vp, _vp, _i64, _vp, _vp,
+                                             _vp, _vp, _vp]
+        L.pmh_sketch_csr_w_async.restype = ctypes.c_int
+        L.pmh_set_weights.argtypes = [_vp, _vp, _i64, _vp, _vp]
+        L.pmh_set_weights.restype = ctypes.c_int
         L.pmh_math_eval.argtypes = [ctypes.c_int, _vp, _i64, _vp, _vp]
         L.pmh_math_eval.restype = ctypes.c_int
         _lib = L

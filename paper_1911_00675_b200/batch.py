@@ -104,12 +104,15 @@ def _stream_ptr(torch, dev):
     return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
 
-def sketch_csr_device(algo, m: int, ids, weights, offsets, want_stats=True):
+def sketch_csr_device(algo, m: int, ids, weights, offsets, want_stats=True, set_weights=None):
     """Device-resident batch sketch.
 
     ids: int64 CUDA tensor [N]; weights: float64 CUDA tensor [N] or None;
-    offsets: int64 CUDA tensor [S+1].  Returns (sig int64 [S, m] CUDA tensor,
-    stats int64 [S, 3] CUDA tensor or None)."""
+    offsets: int64 CUDA tensor [S+1].  set_weights: optional float64 CUDA
+    tensor [S] of the sets' total weights known in advance (the non-streaming
+    form, pmh_sketch_csr_w_async; any positive values give the same
+    signatures).  Returns (sig int64 [S, m] CUDA tensor, stats int64 [S, 3]
+    CUDA tensor or None)."""
     torch = _torch()
     aid = algo_id(algo)
     nsets = offsets.numel() - 1
@@ -119,6 +122,22 @@ def sketch_csr_device(algo, m: int, ids, weights, offsets, want_stats=True):
     if aid in _lib.UNWEIGHTED_IDS:
         weights = None
     _check_device_csr(torch, ids, weights, offsets)
+    if set_weights is not None:
+        if (not isinstance(set_weights, torch.Tensor) or set_weights.dtype != torch.float64
+                or set_weights.device != dev or set_weights.numel() != max(nsets, 0)):
+            raise InvalidParamsError("set_weights must be a float64 tensor of nsets entries on "
+                                     "the batch's device")
+        L = _lib.load()
+        sp = _stream_ptr(torch, dev)
+        status = torch.empty(2, dtype=torch.int64, device=dev)
+        _lib.check(L.pmh_status_reset(status.data_ptr(), sp))
+        _lib.check(L.pmh_sketch_csr_w_async(
+            aid, m, ids.data_ptr(), weights.data_ptr() if weights is not None else None,
+            offsets.data_ptr(), nsets, set_weights.contiguous().data_ptr(), sig.data_ptr(),
+            stats.data_ptr() if stats is not None else None, status.data_ptr(), sp))
+        err = ctypes.c_int64(-1)
+        _lib.check(L.pmh_status_check(status.data_ptr(), ctypes.byref(err), sp), err.value)
+        return sig, stats
     err = ctypes.c_int64(-1)
     rc = _lib.load().pmh_sketch_csr(
         aid, m, ids.data_ptr(), weights.data_ptr() if weights is not None else None,
@@ -159,12 +178,26 @@ def sketch_csr_multi_device(algos, m: int, ids, weights, offsets, want_stats=Fal
     return list(zip(sigs, stats))
 
 
-def sketch_csr(algo, m: int, ids, weights, offsets, want_stats=True):
+def sketch_csr(algo, m: int, ids, weights, offsets, want_stats=True, set_weights=None):
     """Host-array batch sketch -> (sig uint64[S, m], stats int64[S, 3]).
 
-    Goes through the C ABI's host entry point (H2D, kernels, D2H inside)."""
+    Goes through the C ABI's host entry point (H2D, kernels, D2H inside); with
+    set_weights (float64 [S], the sets' total weights known in advance)
+    through the device entry pmh_sketch_csr_w_async."""
     aid = algo_id(algo)
-    _torch()  # a CUDA device is required
+    torch = _torch()  # a CUDA device is required
+    if set_weights is not None:
+        ids_h = np.ascontiguousarray(ids, np.uint64)
+        off_h = np.ascontiguousarray(offsets, np.int64)
+        w_h = None if (aid in _lib.UNWEIGHTED_IDS or weights is None) else \
+            np.ascontiguousarray(weights, np.float64)
+        _check_host_csr(ids_h, w_h, off_h)
+        sw = np.ascontiguousarray(set_weights, np.float64)
+        sig, st = sketch_csr_device(aid, m, to_device_u64(ids_h),
+                                    to_device_f64(w_h) if w_h is not None else None,
+                                    to_device_i64(off_h), want_stats,
+                                    torch.from_numpy(sw).cuda())
+        return sigs_to_numpy(sig), (st.cpu().numpy() if st is not None else None)
     ids = np.ascontiguousarray(ids, np.uint64)
     offsets = np.ascontiguousarray(offsets, np.int64)
     nsets = offsets.size - 1

@@ -513,14 +513,49 @@ int pmh_status_check(const int64_t* d_status, int64_t* err_set, void* stream) {
 static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const double* weights,
                              const int64_t* offsets, int64_t nsets, uint64_t* sig_out,
                              int64_t* stats_out, int64_t* d_status, cudaStream_t st,
-                             int aux_slot);
+                             int aux_slot, const double* setw);
+
+// per-set total weights into a stream-ordered pool buffer (nullptr on error)
+static double* set_weights_tmp(const double* weights, const int64_t* offsets, int64_t nsets,
+                               cudaStream_t st) {
+  double* d = nullptr;
+  if (cudaMallocAsync((void**)&d, sizeof(double) * (size_t)nsets, st) != cudaSuccess) return nullptr;
+  int64_t grid = nsets < 148 * 16 ? nsets : 148 * 16;
+  set_weights_kernel<<<(unsigned)grid, 256, 0, st>>>(weights, offsets, nsets, d);
+  if (cudaGetLastError() != cudaSuccess) { cudaFreeAsync(d, st); return nullptr; }
+  return d;
+}
+
+static bool uses_set_weights(int algo) {
+  return algo == ALG_PMINHASH || algo == ALG_PMH1 || algo == ALG_PMH1A || algo == ALG_PMH2 ||
+         algo == ALG_PMH3 || algo == ALG_PMH3A || algo == ALG_PMH4;
+}
 
 int pmh_sketch_csr_async(int algo, int64_t m, const uint64_t* ids,
                          const double* weights, const int64_t* offsets,
                          int64_t nsets, uint64_t* sig_out, int64_t* stats_out,
                          int64_t* d_status, void* stream) {
   return sketch_async_impl(algo, m, ids, weights, offsets, nsets, sig_out, stats_out, d_status,
-                           (cudaStream_t)stream, 0);
+                           (cudaStream_t)stream, 0, nullptr);
+}
+
+int pmh_sketch_csr_w_async(int algo, int64_t m, const uint64_t* ids, const double* weights,
+                           const int64_t* offsets, int64_t nsets, const double* set_weights,
+                           uint64_t* sig_out, int64_t* stats_out, int64_t* d_status,
+                           void* stream) {
+  return sketch_async_impl(algo, m, ids, weights, offsets, nsets, sig_out, stats_out, d_status,
+                           (cudaStream_t)stream, 0, set_weights);
+}
+
+int pmh_set_weights(const double* weights, const int64_t* offsets, int64_t nsets, double* out,
+                    void* stream) {
+  if (nsets < 0) return set_error(PMH_ERR_INVALID, "negative set count");
+  if (nsets == 0) return PMH_OK;
+  if (!weights || !offsets || !out) return set_error(PMH_ERR_INVALID, "weights, offsets, out required");
+  int64_t grid = nsets < 148 * 16 ? nsets : 148 * 16;
+  set_weights_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(weights, offsets, nsets, out);
+  PMH_CUDA(cudaGetLastError());
+  return PMH_OK;
 }
 
 int pmh_sketch_csr_multi_async(const int* algos, int nalgos, int64_t m, const uint64_t* ids,
@@ -539,6 +574,15 @@ int pmh_sketch_csr_multi_async(const int* algos, int nalgos, int64_t m, const ui
   LanePool* lp = nullptr;
   int rc = get_lanes(nalgos, &lp);
   if (rc) return rc;
+  // the per-set total weights once for every variant (each kernel would
+  // otherwise re-read all weights for its threshold guess)
+  int n_w = 0;
+  for (int k = 0; k < nalgos; k++) n_w += uses_set_weights(algos[k]);
+  double* setw = nullptr;
+  if (weights && n_w > 1) {
+    setw = set_weights_tmp(weights, offsets, nsets, st);
+    if (!setw) return set_error(PMH_ERR_CUDA, "set weights");
+  }
   ForkEvent fork;
   PMH_CUDA(cudaEventRecord(fork.e, st));
   // the P-MinHash-type variants (one long, tail-light kernel) last: their
@@ -552,18 +596,20 @@ int pmh_sketch_csr_multi_async(const int* algos, int nalgos, int64_t m, const ui
   for (int k : order) {
     PMH_CUDA(cudaStreamWaitEvent(lp->s[k], fork.e, 0));
     rc = sketch_async_impl(algos[k], m, ids, weights, offsets, nsets, sig_outs[k],
-                           stats_outs ? stats_outs[k] : nullptr, d_status, lp->s[k], k + 1);
+                           stats_outs ? stats_outs[k] : nullptr, d_status, lp->s[k], k + 1,
+                           uses_set_weights(algos[k]) ? setw : nullptr);
     PMH_CUDA(cudaEventRecord(lp->done[k], lp->s[k]));
     PMH_CUDA(cudaStreamWaitEvent(st, lp->done[k], 0));
-    if (rc != PMH_OK) return rc;
+    if (rc != PMH_OK) { if (setw) cudaFreeAsync(setw, st); return rc; }
   }
+  if (setw) cudaFreeAsync(setw, st);   // after the join: every variant is done with it
   return PMH_OK;
 }
 
 static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const double* weights,
                              const int64_t* offsets, int64_t nsets, uint64_t* sig_out,
                              int64_t* stats_out, int64_t* d_status, cudaStream_t st,
-                             int aux_slot) {
+                             int aux_slot, const double* setw) {
   const int fam = family_of(algo);
   int vrc = validate_sketch(algo, m, weights, nsets);
   if (vrc != PMH_OK) return vrc;
@@ -621,6 +667,7 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
   if (pmin) {
     PMinArgs a{ids, algo == ALG_PMINHASH ? weights : nullptr, offsets, order, nsets, m,
                sig_out, stats_out, d_err_set};
+    a.setw = algo == ALG_PMINHASH ? setw : nullptr;
     if (!pm_split) {
       e = algo == ALG_PMINHASH ? launch_pminhash<true>(a, st) : launch_pminhash<false>(a, st);
     } else {
@@ -644,6 +691,7 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
     a.err_flags = flags;
     a.err_set = d_err_set;
     a.T = *tp;
+    a.setw = is_unweighted(algo) ? nullptr : setw;
     // threshold guess m (ln m + c) / W, measured on config 2 (c = 2/3/4/5):
     // c = 3 best for ProbMinHash 1/2/4 (2-6 % faster PMH2/PMH4 than c = 4;
     // ~5% of sets retry with 4 tg), c = 4 for ProbMinHash 3 (-3% vs 3)
@@ -925,13 +973,22 @@ static int host_multi_impl(const int* algos, int nalgos, int64_t m, const uint64
     cudaStreamWaitEvent(cst[c], ev, 0);
     cudaStreamWaitEvent(cst[c], compute_done, 0);
     const int64_t ns = cut[c + 1] - cut[c];
+    // the chunk's per-set total weights once for its weighted variants
+    int n_w = 0;
+    for (int k = 0; k < nalgos; k++) n_w += chunkable(k) && uses_set_weights(algos[k]);
+    double* setw = nullptr;
+    if (weighted && n_w > 1 && ns > 0) {
+      setw = set_weights_tmp(d_w, d_off + cut[c], ns, cst[c]);
+      if (!setw) { rc = set_error(PMH_ERR_CUDA, "set weights"); break; }
+    }
     for (int k = 0; k < nalgos && rc == PMH_OK && ns > 0; k++) {
       if (!chunkable(k)) continue;
       char* outk = d_out + per_algo * (size_t)k;
       uint64_t* sig0 = (uint64_t*)outk + (size_t)cut[c] * m;
       int64_t* st0 = want_stats ? (int64_t*)(outk + bs) + 3 * cut[c] : nullptr;
-      rc = pmh_sketch_csr_async(algos[k], m, d_ids, weighted ? d_w : nullptr, d_off + cut[c], ns,
-                                sig0, st0, d_status, cst[c]);
+      rc = pmh_sketch_csr_w_async(algos[k], m, d_ids, weighted ? d_w : nullptr, d_off + cut[c], ns,
+                                  uses_set_weights(algos[k]) ? setw : nullptr, sig0, st0, d_status,
+                                  cst[c]);
       if (rc != PMH_OK) break;
       cudaEvent_t evk = mkev();
       cudaEventRecord(evk, cst[c]);
@@ -946,6 +1003,7 @@ static int host_multi_impl(const int* algos, int nalgos, int64_t m, const uint64
         break;
       }
     }
+    if (setw) cudaFreeAsync(setw, cst[c]);
     cudaEvent_t evc = mkev();
     cudaEventRecord(evc, cst[c]);
     chunk_done.push_back(evc);

@@ -257,7 +257,8 @@ template <int F, bool FY16>
 __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, int64_t e0,
                                              int64_t e1, Slot* slots, WarpScratch* wscr,
                                              uint32_t* fy_dense, bool warp_ok, SetShared& sh,
-                                             long long* pts, long long* mul, long long* upd) {
+                                             long long* pts, long long* mul, long long* upd,
+                                             double w_given) {
   const int lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   const int64_t m = a.m;
@@ -274,7 +275,14 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
   for (int64_t L = threadIdx.x; L * 16 < n; L += blockDim.x)
     asm volatile("prefetch.global.L2 [%0];" ::"l"(ids + L * 16));
   double W;
-  if (family_weighted(F) && w) {
+  if (family_weighted(F) && w && w_given > 0.0) {
+    // total weight known in advance (computed once per batch, or the caller's
+    // for the non-streaming variants): no weight pre-pass, the element loop
+    // reads the weights once.  Any W > 0 is exact-safe (it only sizes the
+    // threshold guess that the final verification checks).
+    __syncthreads();
+    W = w_given;
+  } else if (family_weighted(F) && w) {
     // four independent loads in flight per thread (latency-bound otherwise)
     double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
     const int64_t B = blockDim.x;
@@ -395,7 +403,7 @@ __global__ void __launch_bounds__(NT, (NT == SKETCH_THREADS ? SKETCH_MINBLOCKS :
     }
     long long pts = 0, mul = 0, upd = 0;
     const bool failed = sketch_range<F, FY16>(a, off, 0, n, slots, wscr, fy_dense, warp_ok, sh, &pts,
-                                        &mul, &upd);
+                                        &mul, &upd, a.setw ? a.setw[s] : -1.0);
     if (failed && threadIdx.x == 0) {
       atomicOr(a.err_flags, (unsigned long long)ERRF_RANDOMNESS);
       atomicMin(a.err_set, (long long)s);
@@ -433,7 +441,7 @@ __global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS)
   while (split_next_part(sp, &s_t, &p)) {
     long long pts = 0, mul = 0, upd = 0;
     const bool failed = sketch_range<F, FY16>(a, p.off, p.e0, p.e1, slots, wscr, fy_dense, warp_ok, sh,
-                                        &pts, &mul, &upd);
+                                        &pts, &mul, &upd, -1.0);
     if (failed && threadIdx.x == 0) {
       atomicOr(a.err_flags, (unsigned long long)ERRF_RANDOMNESS);
       atomicMin(a.err_set, (long long)p.s);
@@ -530,7 +538,9 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
     const double* w = a.w ? a.w + off : nullptr;
     for (int64_t k = lane; k < m; k += 32) { slots[k].h = EMPTY_H; slots[k].idx = EMPTY_IDX; }
     double W = 0.0;
-    if (family_weighted(F) && w) {
+    if (family_weighted(F) && w && a.setw && a.setw[s] > 0.0) {
+      W = a.setw[s];
+    } else if (family_weighted(F) && w) {
       for (int64_t e = lane; e < n; e += 32) W += w[e];
       for (int o = 16; o > 0; o >>= 1) W += __shfl_xor_sync(0xffffffffu, W, o);
     } else {

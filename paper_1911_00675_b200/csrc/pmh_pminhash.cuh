@@ -32,6 +32,7 @@ struct PMinArgs {
   // order[0, split_info[0]) are split across CTAs (pmh_split.cuh) and skipped
   // by the one-CTA-per-set kernel; nullptr: no split
   const long long* split_info;
+  const double* setw;   // device [nsets] total weights known in advance, or nullptr
 };
 
 constexpr int PMIN_THREADS = 256;
@@ -289,7 +290,7 @@ __device__ __forceinline__ uint64_t add_fma_t(uint64_t st, uint32_t one) {
 template <bool EXPO>
 __device__ __forceinline__ void pm64_range(const PMinArgs& a, int64_t off, int64_t e0, int64_t e1,
                                            Slot* table, unsigned char* smem, uint32_t* s_onep,
-                                           double* s_wsum, int* s_retryp) {
+                                           double* s_wsum, int* s_retryp, double w_given) {
   const int64_t m = a.m;
   const int tpg = (int)(m / PM64_C);               // threads per group
   const int groups = PMIN_THREADS / tpg;
@@ -305,7 +306,10 @@ __device__ __forceinline__ void pm64_range(const PMinArgs& a, int64_t off, int64
   // such a set re-runs with 4 tg, then without a bound.  Draws above tg are
   // never candidates, so no element starts with an infinite threshold.
   double W;
-  if (EXPO && a.w) {
+  if (EXPO && a.w && w_given > 0.0) {
+    W = w_given;   // known in advance (SketchArgs.setw): no weight pre-pass
+    __syncthreads();   // (the pre-pass's barrier also fenced the previous set's table reads)
+  } else if (EXPO && a.w) {
     double p = 0.0;
     for (int64_t k = e0 + threadIdx.x; k < e1; k += blockDim.x) p += __ldg(&a.w[off + k]);
     for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
@@ -462,7 +466,8 @@ __global__ void __launch_bounds__(PMIN_THREADS, PM64_MINBLOCKS) pminhash64_kerne
       if (threadIdx.x == 0) atomicMin(a.err_set, (long long)s);
       continue;
     }
-    pm64_range<EXPO>(a, off, 0, n, table, smem, &s_one, s_wsum, &s_retry);
+    pm64_range<EXPO>(a, off, 0, n, table, smem, &s_one, s_wsum, &s_retry,
+                     a.setw ? a.setw[s] : -1.0);
     uint64_t* sig = a.sig + (size_t)s * m;
     for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
       const unsigned long long bi = table[pm64_slot(k / PM64_C, (int)(k % PM64_C), tpg)].idx;
@@ -500,7 +505,7 @@ __global__ void __launch_bounds__(PMIN_THREADS, PM64_MINBLOCKS)
   if (threadIdx.x == 0) s_one = 1u;
   SplitPart p;
   while (split_next_part(sp, &s_t, &p)) {
-    pm64_range<EXPO>(a, p.off, p.e0, p.e1, table, smem, &s_one, s_wsum, &s_retry);
+    pm64_range<EXPO>(a, p.off, p.e0, p.e1, table, smem, &s_one, s_wsum, &s_retry, -1.0);
     Slot* gt = sp.gtab + (size_t)p.i * m;
     for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
       const Slot v = table[pm64_slot(k / PM64_C, (int)(k % PM64_C), tpg)];

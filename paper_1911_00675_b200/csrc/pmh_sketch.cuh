@@ -345,7 +345,39 @@ struct SketchArgs {
   double tconst;            // threshold-guess constant (ln m + tconst)
   const unsigned* counts;   // device: [0] = number of large sets (order prefix)
   const long long* split_info;  // order[0, split_info[0]) are split (pmh_split.cuh)
+  const double* setw;       // device [nsets] total weights known in advance, or nullptr
 };
+
+// Per-set total weights W_s (one CTA per set, grid-stride): computed once per
+// batch and shared by every variant of a multi-variant call, or supplied by
+// the caller for the non-streaming variants.
+__global__ void __launch_bounds__(256) set_weights_kernel(const double* __restrict__ w,
+                                                          const int64_t* __restrict__ offsets,
+                                                          int64_t nsets, double* __restrict__ out) {
+  __shared__ double red[8];
+  for (int64_t s = blockIdx.x; s < nsets; s += gridDim.x) {
+    const int64_t e0 = offsets[s], e1 = offsets[s + 1];
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+    int64_t e = e0 + threadIdx.x;
+    for (; e + 768 < e1; e += 1024) {
+      p0 += __ldg(&w[e]);
+      p1 += __ldg(&w[e + 256]);
+      p2 += __ldg(&w[e + 512]);
+      p3 += __ldg(&w[e + 768]);
+    }
+    for (; e < e1; e += 256) p0 += __ldg(&w[e]);
+    double v = (p0 + p1) + (p2 + p3);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int i = 0; i < 8; i++) t += red[i];
+      out[s] = t;
+    }
+    __syncthreads();
+  }
+}
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

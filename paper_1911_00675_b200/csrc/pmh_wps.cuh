@@ -130,7 +130,9 @@ __global__ void __launch_bounds__(WPS_THREADS, PMH_WPS_MINB) sketch_wps_kernel(S
     const uint64_t* ids = ws->ids[buf];
     const double* w = ws->w[buf];
     double W = 0.0;
-    if (weighted) {
+    if (weighted && a.setw && a.setw[s] > 0.0) {
+      W = a.setw[s];
+    } else if (weighted) {
       for (int64_t e = lane; e < n; e += 32) W += w[e];
       for (int o = 16; o > 0; o >>= 1) W += __shfl_xor_sync(0xffffffffu, W, o);
     } else {

@@ -4,10 +4,13 @@ CUDA path, plus estimator kernels and size-independent properties at the
 BASELINE.json sizes."""
 import math
 
+import ctypes
+
 import numpy as np
 import pytest
 
 from oracle import oracle as orc
+from paper_1911_00675_b200 import _lib
 from paper_1911_00675_b200 import (
     WEIGHTED_ALGORITHMS, EmptyInputError, InvalidParamsError, TruncExpParams, WeightedSet,
     bbit_reduce, datagen, estimate_pairs, estimate_similarity, estimate_similarity_bbit,
@@ -279,6 +282,33 @@ def test_config4_pareto_m64_subset():
         assert (sigs_to_numpy(sig) != ref).sum() == 0, algo
 
 
+@pytest.mark.parametrize("m", [64, 1024])
+def test_nonstreaming_batch_with_set_weights(m):
+    """sketch_batch("nonstreaming2/4", set_weights=...) through
+    pmh_sketch_csr_w_async: the kernels take the caller's W_s and skip their
+    weight pre-pass; exact W, W off by 10^-3..10^3 (scheduling only: too
+    large costs points, too small forces the verified retry) and the device
+    sums all give the oracle's signatures, on the device and host paths."""
+    import torch
+    b = datagen.config4(nsets=3000, seed=5)
+    W = np.add.reduceat(b.weights, b.offsets[:-1])
+    rng = np.random.default_rng(1)
+    wrong = W * np.exp(rng.uniform(np.log(1e-3), np.log(1e3), W.size))
+    d = _dev(b)
+    L = _lib.load()
+    dev_w = torch.empty(b.nsets, dtype=torch.float64, device="cuda")
+    _lib.check(L.pmh_set_weights(d[1].data_ptr(), d[2].data_ptr(), b.nsets, dev_w.data_ptr(),
+                                 ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    np.testing.assert_allclose(dev_w.cpu().numpy(), W, rtol=1e-12)
+    for algo in ("nonstreaming2", "nonstreaming4"):
+        ref, _ = orc.sketch_csr("probminhash" + algo[-1], m, b.ids, b.weights, b.offsets, threads=16)
+        for sw in (W, wrong, dev_w):
+            sig, _ = sketch_batch(algo, *d, m, set_weights=sw)
+            assert np.array_equal(sigs_to_numpy(sig), ref), (algo, m)
+        sig, _ = sketch_batch(algo, b.ids, b.weights, b.offsets, m, set_weights=wrong)
+        assert np.array_equal(sig, ref), (algo, m, "host")
+
+
 @pytest.mark.parametrize("m", [2, 64, 1024])
 def test_nonstreaming_single_set_api(m):
     """probminhash2/4_nonstreaming == streaming signatures == oracle, with and
@@ -294,7 +324,7 @@ def test_nonstreaming_single_set_api(m):
                          ("probminhash4", probminhash4_nonstreaming)):
             ref, _ = orc.sketch_csr(algo, m, b.ids[lo:hi], b.weights[lo:hi],
                                     np.array([0, hi - lo], np.int64))
-            for tw in (None, W, 1e-3 * W):
+            for tw in (None, W, 1e-3 * W, 1e3 * W):
                 sig, _ = fn(ws, m, total_weight=tw)
                 assert np.array_equal(sig.components, ref[0]), (algo, i, tw)
 

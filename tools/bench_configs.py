@@ -47,13 +47,14 @@ def timed(fn, reps=3):
     return min(ts), float(np.mean(ts))
 
 
-def sketch_fn(algo, m, ids, w, off, S, sig, status):
+def sketch_fn(algo, m, ids, w, off, S, sig, status, setw=None):
     sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
     def f():
-        _lib.check(L.pmh_sketch_csr_async(_lib.ALG[algo], m, ids.data_ptr(),
-                                          w.data_ptr() if w is not None else None, off.data_ptr(),
-                                          S, sig.data_ptr(), None, status.data_ptr(), sp))
+        _lib.check(L.pmh_sketch_csr_w_async(_lib.ALG[algo], m, ids.data_ptr(),
+                                            w.data_ptr() if w is not None else None, off.data_ptr(),
+                                            S, setw.data_ptr() if setw is not None else None,
+                                            sig.data_ptr(), None, status.data_ptr(), sp))
     return f
 
 
@@ -65,9 +66,18 @@ def run_sketch(cfg, batch, algos, m):
     sig = torch.empty((S, m), dtype=torch.int64, device="cuda")
     status = torch.empty(2, dtype=torch.int64, device="cuda")
     out = {}
+    setw = None
+    if any(a.startswith("nonstreaming") for a in algos):
+        # the non-streaming variants: the sets' total weights are known in
+        # advance (computed here, outside the timing, as a caller would have them)
+        setw = torch.empty(S, dtype=torch.float64, device="cuda")
+        _lib.check(L.pmh_set_weights(w.data_ptr(), off.data_ptr(), S, setw.data_ptr(), None))
     for a in algos:
         _lib.check(L.pmh_status_reset(status.data_ptr(), None))
-        tmin, tmean = timed(sketch_fn(a, m, ids, w, off, S, sig, status))
+        ns = a.startswith("nonstreaming")
+        fn = sketch_fn("probminhash" + a[-1] if ns else a, m, ids, w, off, S, sig, status,
+                       setw if ns else None)
+        tmin, tmean = timed(fn)
         err = ctypes.c_int64(-1)
         _lib.check(L.pmh_status_check(status.data_ptr(), ctypes.byref(err), None), err.value)
         line = {"config": cfg, "algo": a, "m": m, "sets": S, "elements": N,
@@ -93,7 +103,7 @@ def main():
         del b
     if "4" in cfgs:
         run_sketch("configs[3] PMH2/PMH4 (non-streaming == streaming) m=64 1e6x100 Pareto1.5",
-                   datagen.config4(), ["probminhash2", "probminhash4"], 64)
+                   datagen.config4(), ["probminhash2", "probminhash4", "nonstreaming2", "nonstreaming4"], 64)
     if "5" in cfgs:
         b, jt, jx = datagen.config5_pairs()
         sig = run_sketch("configs[4] PMH4 m=256 100000x500 (50k pairs)", b, ["probminhash4"], 256)
