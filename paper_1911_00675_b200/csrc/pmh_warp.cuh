@@ -290,24 +290,29 @@ __device__ __forceinline__ double grid_fold(double x0, double d, int lane) {
 #define PMH_GRIDFOLD_FROM 64   // grid_fold for batches starting beyond this point index
 #endif
 
-// Mode B for labels with replacement at label widths kb <= 11 (points of
-// 53 + kb <= 64 bits): a window of 33 stream words always holds 32 whole
-// points, each lane's point lies in two adjacent words (one funnel shift
-// gives its 53 value bits and its label), and ProbMinHash1's running sum
-// folds with grid_fold.  Same results and counters as warp_el_static.
+// Mode B for labels with replacement at label widths kb <= 16 (points of
+// 53 + kb <= 69 bits): a window of 33 (kb <= 11) or 37 stream words always
+// holds 32 whole points, so every batch is 32 points with static offsets;
+// each lane's value bits come from one funnel shift of two adjacent words
+// (the label from the same one when kb <= 11, else from a second), and
+// ProbMinHash1's running sum folds with grid_fold after its first batches.
+// Same results and counters as warp_el_static.
 template <int F>
 __device__ int warp_el_static2(SetCtx& c, const Tables& T, WarpScratch& ws, int lane,
                                int64_t e, uint64_t id, double winv) {
   const uint32_t kb = c.kbits;
   const uint32_t P = 53 + kb;
   const uint64_t kmask = (1ULL << kb) - 1ULL;
+  // window words beyond the first 32: 32 points of P <= 64 bits need 33; of
+  // P <= 69 bits (kb <= 16) 37 (63 + 32 P bits, plus the label funnel's guard)
+  const int nx = kb <= 11 ? 1 : 5;
   uint64_t off = 0;     // absolute bit offset of the next point
   int64_t i = 1;        // next point index (1-based)
   double x = 0.0;       // PMH1 running sum
   for (;;) {
     const uint64_t wb = off >> 6;
     ws.words[lane] = stream_word(id, wb + 1 + (uint64_t)lane);
-    if (lane == 0) ws.words[32] = stream_word(id, wb + 33);
+    if (lane < nx) ws.words[32 + lane] = stream_word(id, wb + 33 + (uint64_t)lane);
     __syncwarp();
     const uint32_t rel0 = (uint32_t)(off & 63);
     const double thr = warp_thr(c);
@@ -317,7 +322,14 @@ __device__ int warp_el_static2(SetCtx& c, const Tables& T, WarpScratch& ws, int 
     const uint64_t w0 = ws.words[wi];
     const uint64_t v = sh ? (w0 >> sh) | (ws.words[wi + 1] << (64 - sh)) : w0;
     const uint64_t u = v & ((1ULL << 53) - 1ULL);
-    int32_t lab = (int32_t)((v >> 53) & kmask) + 1;
+    int32_t lab;
+    if (kb <= 11) {   // the label is in the same 64 bits
+      lab = (int32_t)((v >> 53) & kmask) + 1;
+    } else {
+      const uint32_t rl = ro + 53, wl = rl >> 6, sl = rl & 63;
+      const uint64_t l0 = ws.words[wl];
+      lab = (int32_t)(((sl ? (l0 >> sl) | (ws.words[wl + 1] << (64 - sl)) : l0)) & kmask) + 1;
+    }
     double xv = 0.0;
     uint32_t ncand = 32;
     bool had_slow = false;
@@ -577,6 +589,49 @@ __device__ void parse_fy_parallel(const SetCtx& c, WarpScratch& ws, uint64_t id,
   __syncwarp();
 }
 
+// The common case of a Fisher-Yates batch: no label draw of the batch's run
+// is rejected, so every point sits at its static offset rel0 + k (53 + kb).
+// Loads the window's first 37 words (enough for 32 static points of <= 69
+// bits), checks each lane's first label field against its range R (K:97-110)
+// and, if all accept, writes the parse result.  Returns false -- the caller
+// then loads the rest of the 64-word window and runs parse_fy_parallel -- on
+// any rejection, for the last point (R = 1) or for kb > 16.  (At m = 4096
+// the first ~40 ranges reject with probability < 1%.)
+__device__ __forceinline__ bool parse_fy_fast(const SetCtx& c, WarpScratch& ws, uint64_t id,
+                                              uint64_t off, int64_t i0, int lane) {
+  const int64_t m = c.m;
+  const uint64_t wb = off >> 6;
+  ws.words[lane] = stream_word(id, wb + 1 + (uint64_t)lane);
+  if (lane < 5) ws.words[32 + lane] = stream_word(id, wb + 33 + (uint64_t)lane);
+  __syncwarp();
+  const int64_t R0 = m - i0 + 1;
+  if (R0 <= 1) return false;
+  const uint32_t kb = bits_for_fast(R0);
+  if (kb > 16) return false;
+  const uint32_t P = 53u + kb;
+  const uint32_t rel0 = (uint32_t)(off - (wb << 6));
+  const int64_t R = m - (i0 + lane) + 1;
+  const bool inrun = R > 1 && bits_for_fast(R) == kb;
+  const unsigned runmask = __ballot_sync(0xffffffffu, inrun);
+  const uint32_t qmax = runmask == 0xffffffffu ? 32u : (uint32_t)(__ffs(~runmask) - 1);
+  const uint32_t ro = rel0 + (uint32_t)lane * P;
+  const bool mine = (uint32_t)lane < qmax;
+  uint32_t field = 0;
+  if (mine) field = (uint32_t)win_bits(ws.words, ro + 53u, kb);
+  if (__ballot_sync(0xffffffffu, mine && !((int64_t)field < R))) return false;
+  if (mine) {
+    ws.eoff[lane] = ro;
+    ws.lab[lane] = (int32_t)field;   // the FY index; the label after fy_steps
+  }
+  if (lane == 0) {
+    ws.q = qmax;
+    ws.flags = 0;
+    ws.next_off = (wb << 6) + rel0 + (uint64_t)qmax * P;
+  }
+  __syncwarp();
+  return true;
+}
+
 // Warp-parallel lazy Fisher-Yates for the q points of a batch (lane k =
 // point pt_k = i0 + k with index j_k = pt_k + r_k, K:222-235).  Sequentially:
 //   out_k = P[j_k];  P[j_k] = P[pt_k]
@@ -638,8 +693,12 @@ __device__ int warp_el_fy(SetCtx& c, const Tables& T, WarpScratch& ws, uint32_t*
   double x = 0.0;
   for (;;) {
     const uint64_t wb = off >> 6;
-    win_load64(ws, id, wb, lane);
-    parse_fy_parallel(c, ws, id, off, i, lane);
+    if (!parse_fy_fast(c, ws, id, off, i, lane)) {
+      // a rejection in the batch: the rest of the 64-word window, full parse
+      if (lane < 28) ws.words[37 + lane] = stream_word(id, wb + 38 + (uint64_t)lane);
+      __syncwarp();
+      parse_fy_parallel(c, ws, id, off, i, lane);
+    }
     if (ws.flags & 2u) return EL_FAIL;
     uint32_t q = ws.q;
     const int64_t pt = i + lane;
@@ -722,7 +781,7 @@ __device__ __forceinline__ int warp_element(SetCtx& c, const Tables& T, WarpScra
 #ifndef PMH_STATIC2
 #define PMH_STATIC2 1
 #endif
-    if (PMH_STATIC2 && c.kbits <= 11) return warp_el_static2<F>(c, T, ws, lane, e, id, winv);
+    if (PMH_STATIC2 && c.kbits <= 16) return warp_el_static2<F>(c, T, ws, lane, e, id, winv);
     return warp_el_static<F>(c, T, ws, lane, e, id, winv);
   }
   else
