@@ -83,6 +83,10 @@ UNIT = "elements/s"
 # (ProbMinHash 1/1a/2) or TruncExp points (3/3a/4)
 POINT_KIND = {"probminhash1": 0, "probminhash1a": 0, "probminhash2": 0,
               "probminhash3": 1, "probminhash3a": 1, "probminhash4": 1}
+# c_v of SURVEY.md §8d: SASS instructions (issue slots) per point of the
+# per-point probe's loop body, by point kind (tools/sass_loop_cost.py ->
+# profiles/r02_point_cost_sass.txt): a log1p point 270, a TruncExp point 81
+C_V = {0: 270, 1: 81}
 
 
 def _peaks():
@@ -546,8 +550,11 @@ def run_config2(args, ctx):
         if v in POINT_KIND and v in pmin:
             rate = pmin[v] / (t / 1e3) / 1e9
             ceil = peaks["point_rate_gpts"]["log1p" if POINT_KIND[v] == 0 else "truncexp"]
+            cv = C_V[POINT_KIND[v]]
+            issue = pmin[v] * cv / (t / 1e3) / 1e9
             d.update({"points_min": pmin[v], "points_min_gpts": rate,
-                      "point_rate_peak_gpts": ceil, "point_frac": rate / ceil})
+                      "point_rate_peak_gpts": ceil, "point_frac": rate / ceil,
+                      "c_v": cv, "issue_gops": issue, "issue_frac": issue / peaks["ffma_gops"]})
             d["bound"] = "points" if d["point_frac"] >= d["hbm_frac"] else "hbm"
         elif v == "pminhash":
             alu = float(N) * M * ALU_OPS_PER_DRAW / (t / 1e3) / 1e9
