@@ -17,7 +17,7 @@ def main(src, dst, header):
         ns = v * {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6,
                   "nsecond": 1}.get(unit, 1)
         rows.append((r["Kernel Name"], ns))
-    step = [r for r in rows if not r[0].startswith("alu_probe")]
+    step = [r for r in rows if "probe_kernel" not in r[0] and not r[0].startswith("alu_probe")]
     tot = sum(ns for _, ns in step)
     with open(dst, "w") as f:
         f.write(header.rstrip() + "\n")

@@ -23,3 +23,13 @@ python tools/ncu_driver.py pminhash > /dev/null 2>&1 && \
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:pminhash64 -c 1 \
     -f -o gpurun_out/pm64_$TAG python tools/ncu_driver.py pminhash > gpurun_out/ncu_pm64_$TAG.log 2>&1
 echo "ncu full rc=$?"
+# configs[4] end to end (NCCL path) and the ProbMinHash kernels of one step
+timeout 600 python bench.py --workload config5 --steps 3 --warmup 1 > gpurun_out/bench_cfg5_$TAG.json 2> gpurun_out/bench_cfg5_$TAG.err
+echo "config5 rc=$?"
+python tools/ncu_driver_cfg.py config4 probminhash4 64 200000 > /dev/null 2>&1 && \
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:sketch_wps -c 1 \
+    -f -o gpurun_out/wps_$TAG python tools/ncu_driver_cfg.py config4 probminhash4 64 200000 > gpurun_out/ncu_wps_$TAG.log 2>&1
+echo "ncu wps rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"sketch_sets|sketch_small" \
+    -f -o gpurun_out/pmh_$TAG python tools/ncu_driver.py probminhash4 > gpurun_out/ncu_pmh_$TAG.log 2>&1
+echo "ncu pmh4 rc=$?"
