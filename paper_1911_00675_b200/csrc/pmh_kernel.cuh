@@ -304,12 +304,12 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
   c.slots = slots;
   c.hmax_bits = &sh.hmax;
   c.filled = &sh.filled;
-  c.m = m;
+  c.m = (int32_t)m;
   c.kbits = bits_for(m);
-  c.cap = coupon_cap(m);
+  c.cap = (int32_t)coupon_cap(m);
   c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
   c.trig = false;
-  c.eoff = e0;
+  c.eoff = (int32_t)e0;
   double tg = (double)m * (log((double)m) + a.tconst) / W;
   if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
   bool failed = false;
@@ -552,9 +552,9 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
     c.slots = slots;
     c.hmax_bits = &wv->hmax;
     c.filled = &wv->filled;
-    c.m = m;
+    c.m = (int32_t)m;
     c.kbits = bits_for(m);
-    c.cap = coupon_cap(m);
+    c.cap = (int32_t)coupon_cap(m);
     c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
   c.trig = false;
     c.eoff = 0;

@@ -36,24 +36,28 @@ struct Tables {
   const double* beta;         // PMH2: [m+1], beta_i = m/(m-i+1.0)
 };
 
+// 32-bit fields where the ranges allow (m <= 65535, coupon cap < 2^31,
+// per-thread counters, in-set element indices < 2^31): the state lives in
+// registers across the element loops, and 64-bit fields pushed the 80-register
+// kernels into rematerialising and spilling
 struct SetCtx {
   Slot* slots;                       // [m] shared
   unsigned long long* hmax_bits;     // shared, current upper bound of H
   unsigned int* filled;              // shared, #non-empty slots
   double tguess;                     // current threshold guess
-  int64_t m;
+  int32_t m;
   uint32_t kbits;
-  int64_t cap;                       // coupon cap K:279-281
+  int32_t cap;                       // coupon cap K:279-281
   // counters (per thread)
-  int64_t points;
+  uint32_t points;
   double tprev;                      // previous attempt's threshold (-1: none);
                                      // a retry counts only points above it
-  int64_t updates;
-  int64_t multi;                     // elements that produced > 1 point
+  uint32_t updates;
+  uint32_t multi;                    // elements that produced > 1 point
   int since_refresh;                 // batches since the last h_max refresh
   bool trig;                         // this lane lowered the maximum slot / filled the last
                                      // one: the warp refreshes h_max after the batch
-  int64_t eoff;                      // in-set index of element 0 (a split set's part)
+  int32_t eoff;                      // in-set index of element 0 (a split set's part)
 };
 
 __device__ __forceinline__ double ctx_thr(const SetCtx& c) {

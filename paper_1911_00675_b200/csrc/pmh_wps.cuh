@@ -142,9 +142,9 @@ __global__ void __launch_bounds__(WPS_THREADS, PMH_WPS_MINB) sketch_wps_kernel(S
     c.slots = ws->slots;
     c.hmax_bits = &ws->hmax;
     c.filled = &ws->filled;
-    c.m = m;
+    c.m = (int32_t)m;
     c.kbits = bits_for(m);
-    c.cap = coupon_cap(m);
+    c.cap = (int32_t)coupon_cap(m);
     c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
     c.trig = false;
     c.eoff = 0;

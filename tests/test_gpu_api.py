@@ -241,6 +241,23 @@ def test_config2_subset_all_variants_bit_exact():
     assert (sigs_to_numpy(sig) != ref).sum() == 0
 
 
+def test_config2_pminhash_reference_sample_bit_exact():
+    """configs[1] P-MinHash at m=1024 on the reference arm's 137-set stratified
+    sample (1.14M elements, sizes 1..10^5, the largest sets split across CTAs
+    on the GPU) against the oracle's equal-cost parallel run."""
+    import os
+    full = datagen.config2()
+    sizes = np.diff(full.offsets)
+    order = np.argsort(sizes, kind="stable")
+    k = int(np.ceil(sizes.sum() / 1_200_000))
+    sub = full.subset(np.sort(order[::k]))
+    assert sub.nelems > 1_000_000
+    sig, _ = sketch_batch("pminhash", *_dev(sub), 1024)
+    ref = orc.sketch_csr_balanced("pminhash", 1024, sub.ids, sub.weights, sub.offsets,
+                                  threads=os.cpu_count() or 8)
+    assert (sigs_to_numpy(sig) != ref).sum() == 0
+
+
 def test_config2_full_properties():
     """Full configs[1] batch: permutation invariance within sets, power-of-two
     scale invariance and determinism (size-independent properties)."""
