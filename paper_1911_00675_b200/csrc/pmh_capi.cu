@@ -20,6 +20,7 @@
 #include "../../include/pmh.h"
 #include "pmh_pminhash.cuh"
 #include "pmh_kernel.cuh"
+#include "pmh_flat.cuh"
 #include "pmh_order.cuh"
 #include "pmh_probe.cuh"
 #include "pmh_baselines.cuh"
@@ -658,8 +659,16 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
   const bool pm_split = pm_static && split_n >= 64 && (split_n & (split_n - 1)) == 0 &&
                         split_cap > 0;
   OrderWs ow;
+#ifndef PMH_FLAT
+#define PMH_FLAT 1
+#endif
+  // ProbMinHash3 / unweighted 3 at power-of-two m: the flat point-parallel
+  // kernel takes the sets up to PMH_FLAT_NMAX elements (instead of the
+  // warp-per-set kernels), concurrently with the CTA kernel on the larger ones
+  const bool flat = PMH_FLAT && !pmin && flat_eligible(fam, m);
   // cost offset: ProbMinHash families pay ~m ln m points per set regardless of n
-  e = build_order(offsets, nsets, pmin ? 0 : (int64_t)(PMH_ORDER_COST_M * (double)m), pmin ? -1 : small_n_for(fam, m),
+  e = build_order(offsets, nsets, pmin ? 0 : (int64_t)(PMH_ORDER_COST_M * (double)m),
+                  pmin ? -1 : (flat ? (int64_t)PMH_FLAT_NMAX : small_n_for(fam, m)),
                   pm_split ? split_n : 4096, st, &ow);
   if (e != cudaSuccess) return cuda_fail(e, "set ordering");
   int32_t* order = ow.order;
@@ -769,8 +778,17 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
       }
     };
     const bool do_split = sp_n >= 64 && sp_cap > 0;
+    auto flat_launch = [&]() -> cudaError_t {   // the small partition, on the aux stream
+      const size_t smem = sizeof(Slot) * (size_t)m;
+      auto kern = fam == FAM_PMH3 ? sketch_flat_kernel<FAM_PMH3> : sketch_flat_kernel<FAM_UW3>;
+      cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e2 != cudaSuccess) return e2;
+      int64_t grid = nsets < 148 * 6 ? nsets : 148 * 6;
+      kern<<<(unsigned)grid, FLAT_THREADS, smem, aux->s>>>(a);
+      return cudaGetLastError();
+    };
     // the small-set kernel first (see get_aux)
-    e = small();
+    e = flat ? flat_launch() : small();
     if (e == cudaSuccess && do_split) e = split();
     if (e == cudaSuccess) e = big();
     cudaEventRecord(aux->join, aux->s);
