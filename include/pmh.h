@@ -193,6 +193,21 @@ int pmh_allpairs_hist(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0, in
                       int64_t c0, int64_t c1, int32_t thr, uint64_t* hist, uint64_t* pairs,
                       int64_t cap, uint64_t* cursor, void* stream);
 
+/*
+ * The same reduction by an exact hash join on (component, value)
+ * (csrc/pmh_join.cuh): only the pairs sharing a component are ever visited,
+ * so a batch whose sets rarely share components (configs[4]) costs O(n m)
+ * instead of O(n^2 m).  Same histogram and pair set as pmh_allpairs_hist
+ * (thr >= 1).  Synchronises the stream once (the work check).  Returns 1 --
+ * nothing written -- when the pairs sharing a key exceed max_visits (<= 0:
+ * 2^26; e.g. many duplicate sets) or thr <= 0; the caller then runs
+ * pmh_allpairs_hist.  Stream-ordered temporaries from the device pool (up to
+ * ~1.5 GB of tables plus the pair map).
+ */
+int pmh_allpairs_join_hist(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0, int64_t r1,
+                           int64_t c0, int64_t c1, int32_t thr, uint64_t* hist, uint64_t* pairs,
+                           int64_t cap, uint64_t* cursor, int64_t max_visits, void* stream);
+
 /* b-bit reduction of nsets*m components (estimate.py:105-114, K:851-861). */
 int pmh_bbit(const uint64_t* sig, int64_t nsets, int64_t m, int b,
              int64_t* out, void* stream);

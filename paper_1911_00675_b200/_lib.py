@@ -41,7 +41,7 @@ EXPORTS = ("pmh_version", "pmh_last_error", "pmh_sketch_csr", "pmh_sketch_csr_as
            "pmh_bbit_words", "pmh_bbit_pack", "pmh_allpairs_bbit_hist",
            "pmh_mse_cell", "pmh_parse_weighted_text", "pmh_probe_alu_peak",
            "pmh_probe_pipe_peak", "pmh_probe_point_rate", "pmh_math_eval",
-           "pmh_sketch_csr_w_async", "pmh_set_weights")
+           "pmh_sketch_csr_w_async", "pmh_set_weights", "pmh_allpairs_join_hist")
 
 _lib = None
 _lock = threading.Lock()
@@ -126,6 +126,9 @@ def load():
         L.pmh_sketch_csr_w_async.restype = ctypes.c_int
         L.pmh_set_weights.argtypes = [_vp, _vp, _i64, _vp, _vp]
         L.pmh_set_weights.restype = ctypes.c_int
+        L.pmh_allpairs_join_hist.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, _i64,
+                                             ctypes.c_int32, _vp, _vp, _i64, _vp, _i64, _vp]
+        L.pmh_allpairs_join_hist.restype = ctypes.c_int
         L.pmh_math_eval.argtypes = [ctypes.c_int, _vp, _i64, _vp, _vp]
         L.pmh_math_eval.restype = ctypes.c_int
         _lib = L

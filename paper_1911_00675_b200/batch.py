@@ -273,10 +273,15 @@ def allpairs_tile_device(sigs, r0, r1, c0, c1, out=None):
 
 
 def allpairs_hist_device(sigs, r0=0, r1=None, c0=0, c1=None, threshold=1, cap=1 << 22,
-                         hist=None):
+                         hist=None, method="dense", max_visits=0):
     """Histogram (int64 [m+1], CUDA) of equal-component counts over the pairs
     (i, j), j > i, of rows [r0,r1) x cols [c0,c1), plus the pairs with count >=
-    threshold: returns (hist, pairs int64 [K, 3] numpy (i, j, count), total K)."""
+    threshold: returns (hist, pairs int64 [K, 3] numpy (i, j, count), total K).
+
+    method: "dense" compares every pair (pmh_allpairs_hist); "join" visits only
+    the pairs sharing a (component, value) key (pmh_allpairs_join_hist; raises
+    if it declines); "auto" tries the join and falls back to dense when the
+    key lists are too long.  All give the same histogram and pair set."""
     torch = _torch()
     n, m = sigs.shape
     r1 = n if r1 is None else r1
@@ -285,9 +290,21 @@ def allpairs_hist_device(sigs, r0=0, r1=None, c0=0, c1=None, threshold=1, cap=1 
         hist = torch.zeros(m + 1, dtype=torch.int64, device=sigs.device)
     pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=sigs.device)
     cursor = torch.zeros(1, dtype=torch.int64, device=sigs.device)
-    rc = _lib.load().pmh_allpairs_hist(sigs.contiguous().data_ptr(), n, m, r0, r1, c0, c1,
-                                       int(threshold), hist.data_ptr(), pairs.data_ptr(), cap,
-                                       cursor.data_ptr(), _stream_ptr(torch, sigs.device))
+    L = _lib.load()
+    sp = _stream_ptr(torch, sigs.device)
+    sg = sigs.contiguous()
+    rc = 1
+    if method in ("join", "auto") and int(threshold) >= 1:
+        rc = L.pmh_allpairs_join_hist(sg.data_ptr(), n, m, r0, r1, c0, c1, int(threshold),
+                                      hist.data_ptr(), pairs.data_ptr(), cap, cursor.data_ptr(),
+                                      int(max_visits), sp)
+        if rc == 1 and method == "join":
+            raise InvalidParamsError("join declined: too many pairs share a component")
+    elif method not in ("dense", "auto"):
+        raise InvalidParamsError(f"unknown all-pairs method {method!r}")
+    if rc == 1:
+        rc = L.pmh_allpairs_hist(sg.data_ptr(), n, m, r0, r1, c0, c1, int(threshold),
+                                 hist.data_ptr(), pairs.data_ptr(), cap, cursor.data_ptr(), sp)
     _lib.check(rc)
     k = int(cursor.item())
     return hist, _pairs_out(pairs, k, cap), k

@@ -21,6 +21,7 @@
 #include "pmh_pminhash.cuh"
 #include "pmh_kernel.cuh"
 #include "pmh_flat.cuh"
+#include "pmh_join.cuh"
 #include "pmh_order.cuh"
 #include "pmh_probe.cuh"
 #include "pmh_baselines.cuh"
@@ -1202,6 +1203,101 @@ int pmh_allpairs_hist(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0, in
                                   cursor, (cudaStream_t)stream);
   return launch_allpairs_exact2(sigs, m, r0, r1, c0, c1, thr, hist, pairs, cap, cursor,
                                 (cudaStream_t)stream);
+}
+
+// pmh_join.cuh: exact all-pairs histogram by a (component, value) hash join.
+// Returns 1 (declined, nothing written) when the key lists exceed the work
+// budget or thr <= 0; the caller then runs pmh_allpairs_hist.
+__global__ void join_map_init_kernel(PairSlot* map, int64_t slots) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < slots;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    map[s].key = PAIR_EMPTY;
+    map[s].cnt = 0ULL;
+  }
+}
+
+int pmh_allpairs_join_hist(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0, int64_t r1,
+                           int64_t c0, int64_t c1, int32_t thr, uint64_t* hist, uint64_t* pairs,
+                           int64_t cap, uint64_t* cursor, int64_t max_visits, void* stream) {
+  if (m < 1 || m > 65535 || r0 < 0 || r1 > n || c0 < 0 || c1 > n || r0 > r1 || c0 > c1)
+    return set_error(PMH_ERR_INVALID, "bad tile bounds");
+  if (n >= (1LL << 31)) return set_error(PMH_ERR_INVALID, "n must be < 2^31");
+  if (r0 == r1 || c0 == c1) return PMH_OK;
+  if (thr <= 0) return 1;   // zero-count pairs would have to be listed
+  cudaStream_t st = (cudaStream_t)stream;
+  int logC = 10;
+  while ((1LL << logC) < 2 * n) logC++;
+  const size_t per_comp = (sizeof(JoinSlot) + sizeof(int32_t)) << logC;
+  const size_t budget = (size_t)1536 << 20;   // table memory per component group
+  int64_t G = (int64_t)(budget / (per_comp + sizeof(int32_t) * (size_t)n));
+  G = G < 1 ? 1 : (G > m ? m : G);
+  const int64_t groups = (m + G - 1) / G;
+  if (max_visits <= 0) max_visits = 1LL << 26;
+  char* ws = nullptr;
+  const size_t b_tab = sizeof(JoinSlot) * ((size_t)G << logC), b_head = sizeof(int32_t) * ((size_t)G << logC),
+               b_next = sizeof(int32_t) * (size_t)n * (size_t)G;
+  PMH_CUDA(cudaMallocAsync((void**)&ws, b_tab + b_head + b_next + 64, st));
+  JoinSlot* tab = (JoinSlot*)ws;
+  int32_t* head = (int32_t*)(ws + b_tab);
+  int32_t* next = (int32_t*)(ws + b_tab + b_head);
+  unsigned long long* ctr = (unsigned long long*)(ws + b_tab + b_head + b_next);   // visits, occ
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)(sms * 8);
+  auto build = [&](int64_t g) -> cudaError_t {
+    const int64_t k0 = g * G, gg = (m - k0) < G ? (m - k0) : G;
+    cudaError_t e = cudaMemsetAsync(tab, 0, sizeof(JoinSlot) * ((size_t)gg << logC), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(head, 0xFF, sizeof(int32_t) * ((size_t)gg << logC), st);
+    if (e != cudaSuccess) return e;
+    join_insert_kernel<<<grid, 256, 0, st>>>(sigs, n, m, k0, gg, tab, head, next, logC);
+    return cudaGetLastError();
+  };
+  auto group_g = [&](int64_t g) { const int64_t k0 = g * G; return (m - k0) < G ? (m - k0) : G; };
+  int rc = PMH_OK;
+  cudaError_t e = cudaMemsetAsync(ctr, 0, 16, st);
+  for (int64_t g = 0; g < groups && e == cudaSuccess; g++) {
+    e = build(g);
+    if (e == cudaSuccess) {
+      join_emit_kernel<<<grid, 256, 0, st>>>(next, n, group_g(g), r0, r1, c0, c1, ctr, nullptr, 0);
+      e = cudaGetLastError();
+    }
+  }
+  unsigned long long visits = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&visits, ctr, 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) { cudaFreeAsync(ws, st); return cuda_fail(e, "join count"); }
+  if ((long long)visits > max_visits) { cudaFreeAsync(ws, st); return 1; }
+  int logM = 10;
+  while ((1ULL << logM) < 2 * visits) logM++;
+  PairSlot* map = nullptr;
+  e = cudaMallocAsync((void**)&map, sizeof(PairSlot) << logM, st);
+  if (e != cudaSuccess) { cudaFreeAsync(ws, st); return cuda_fail(e, "join map"); }
+  join_map_init_kernel<<<grid, 256, 0, st>>>(map, 1LL << logM);
+  for (int64_t g = 0; g < groups && e == cudaSuccess; g++) {
+    if (groups > 1) e = build(g);   // one group: the tables of the count pass are still there
+    if (e == cudaSuccess) {
+      join_emit_kernel<<<grid, 256, 0, st>>>(next, n, group_g(g), r0, r1, c0, c1, nullptr, map, logM);
+      e = cudaGetLastError();
+    }
+  }
+  // pairs in range: a in [r0, r1), b in [c0, c1), b > a
+  unsigned long long in_range = 0;
+  for (int64_t a = r0; a < r1; a++) {
+    const int64_t lo = c0 > a + 1 ? c0 : a + 1;
+    if (c1 > lo) in_range += (unsigned long long)(c1 - lo);
+  }
+  if (e == cudaSuccess) {
+    join_scan_kernel<<<grid, 256, 0, st>>>(map, 1LL << logM, m, thr, (unsigned long long*)hist,
+                                           (unsigned long long*)pairs, cap,
+                                           (unsigned long long*)cursor, ctr + 1);
+    join_zeros_kernel<<<1, 1, 0, st>>>((unsigned long long*)hist, ctr + 1, in_range);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(map, st);
+  cudaFreeAsync(ws, st);
+  if (e != cudaSuccess) rc = cuda_fail(e, "join");
+  return rc;
 }
 
 int64_t pmh_bbit_words(int64_t m, int b) {

@@ -113,6 +113,7 @@ class AllPairsResult:
     pairs: np.ndarray         # int64[K, 3]: (i, j, count) with count >= threshold
     tiles: int
     total: int = -1           # pairs with count >= threshold found (== len(pairs))
+    rows: list = None         # [(r0, r1)]: the pair rows (smaller index) this rank covered
 
 
 def allpairs_local(sigs_all, rows, tile, threshold, count_tile_fn):
@@ -140,7 +141,8 @@ def allpairs_local(sigs_all, rows, tile, threshold, count_tile_fn):
                 found.append(np.stack([iw + r0, jw + c0, cnt[sel]], axis=1).astype(np.int64))
             tiles += 1
     pairs = np.concatenate(found) if found else np.zeros((0, 3), np.int64)
-    return AllPairsResult(hist, pairs, tiles, len(pairs))
+    return AllPairsResult(hist, pairs, tiles, len(pairs),
+                          [(b * tile, min(n, (b + 1) * tile)) for b in rows])
 
 
 def _gpu_count_tile(sigs_all, r0, r1, c0, c1):
@@ -176,7 +178,45 @@ def _gpu_rows_hist(sigs_all, rows, tile, threshold, cap=1 << 22):
         total += k
         found.append(pairs)
     pairs = np.concatenate(found) if found else np.zeros((0, 3), np.int64)
-    return AllPairsResult(hist.cpu().numpy(), pairs, len(rows), total)
+    return AllPairsResult(hist.cpu().numpy(), pairs, len(rows), total,
+                          [(b * tile, min(n, (b + 1) * tile)) for b in rows])
+
+
+def triangle_rows(n: int, world: int):
+    """Contiguous row ranges [(r0, r1)] per rank with near-equal upper-triangle
+    pair counts (row i holds n - 1 - i pairs)."""
+    cum = np.concatenate([[0], np.cumsum(np.arange(n - 1, -1, -1, dtype=np.float64))])
+    total = cum[-1]
+    b = [0] + [int(np.searchsorted(cum, total * r / world, side="left")) for r in range(1, world)] + [n]
+    for r in range(1, world + 1):
+        b[r] = max(b[r], b[r - 1])
+    return [(b[r], b[r + 1]) for r in range(world)]
+
+
+def _gpu_rows_join(sigs_all, rank, world, threshold, cap=1 << 22):
+    """This rank's contiguous triangle rows by the (component, value) hash join
+    (pmh_allpairs_join_hist), one call; None if the join declines."""
+    import torch
+    from . import _lib
+    from .batch import _pairs_out, _stream_ptr
+    n, m = sigs_all.shape
+    r0, r1 = triangle_rows(n, world)[rank]
+    hist = torch.zeros(m + 1, dtype=torch.int64, device=sigs_all.device)
+    while True:
+        pairs = torch.empty((max(cap, 1), 2), dtype=torch.int64, device=sigs_all.device)
+        cursor = torch.zeros(1, dtype=torch.int64, device=sigs_all.device)
+        rc = _lib.load().pmh_allpairs_join_hist(
+            sigs_all.data_ptr(), n, m, r0, r1, 0, n, int(threshold), hist.data_ptr(),
+            pairs.data_ptr(), cap, cursor.data_ptr(), 0, _stream_ptr(torch, sigs_all.device))
+        if rc == 1:
+            return None
+        _lib.check(rc)
+        k = int(cursor.item())
+        if k <= cap:
+            break
+        hist.zero_()
+        cap = k          # the list overflowed: once more with room for all
+    return AllPairsResult(hist.cpu().numpy(), _pairs_out(pairs, k, cap), 1, k, [(r0, r1)])
 
 
 def _stamp(dev):
@@ -188,7 +228,7 @@ def _stamp(dev):
 
 
 def allpairs_distributed(local_sigs, rank, world, tile=4096, threshold=1, group=None,
-                         count_tile_fn=None, cap=1 << 22, ms=None):
+                         count_tile_fn=None, cap=1 << 22, ms=None, method="auto"):
     """All-gather the sharded signatures, compute this rank's block rows and
     all_reduce the histogram.  local_sigs: torch tensor [n_r, m] (int64, on
     the rank's device for NCCL; CPU for gloo).  Ranks may hold different row
@@ -214,7 +254,15 @@ def allpairs_distributed(local_sigs, rank, world, tile=4096, threshold=1, group=
     n = sigs_all.shape[0]
     rows = block_rows(n, tile, world)[rank]
     if count_tile_fn is None:
-        res = _gpu_rows_hist(sigs_all, rows, tile, threshold, cap)
+        res = None
+        if method in ("join", "auto") and threshold >= 1:
+            # contiguous triangle rows by the hash join (a few ms at configs[4]);
+            # the dense block rows when the join declines
+            res = _gpu_rows_join(sigs_all.contiguous(), rank, world, threshold, cap)
+            if res is None and method == "join":
+                raise RuntimeError("all-pairs join declined")
+        if res is None:
+            res = _gpu_rows_hist(sigs_all, rows, tile, threshold, cap)
     else:
         res = allpairs_local(sigs_all, rows, tile, threshold, count_tile_fn)
     t2 = _stamp(dev)

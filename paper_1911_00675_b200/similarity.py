@@ -141,7 +141,7 @@ def _sync(device):
 
 def run_pairs(batch, jtarget, jexact, m: int, rank: int = 0, world: int = 1, group=None,
               algo: str = "probminhash4", tile: int = 4096, sketch_fn=None,
-              count_tile_fn=None) -> PairsRunResult:
+              count_tile_fn=None, method: str = "auto") -> PairsRunResult:
     """The configs[4] pipeline on this rank (every rank calls it with the same
     batch; ranks > 0 may pass world > 1 only inside an initialised process
     group).  Returns the reduced per-bucket statistics (identical on every
@@ -185,13 +185,16 @@ def run_pairs(batch, jtarget, jexact, m: int, rank: int = 0, world: int = 1, gro
     inner = {}
     res = stage("allpairs", lambda: pdist.allpairs_distributed(
         local, rank, world, tile=tile, threshold=1, group=group,
-        count_tile_fn=count_tile_fn, ms=inner), dev)
+        count_tile_fn=count_tile_fn, ms=inner, method=method), dev)
     ms.update({"allpairs." + k: v for k, v in inner.items()})
     # each designed pair (2p, 2p+1) lies in exactly one block row; pairs of
     # the rows this rank computed are in its list
     counts, extra = designed_counts(res.pairs, 0, npairs)
-    rows = pdist.block_rows(2 * npairs, tile, world)[rank]
-    mine = np.isin((2 * np.arange(npairs)) // tile, rows)
+    # the designed pairs whose first set lies in the rows this rank covered
+    first = 2 * np.arange(npairs)
+    mine = np.zeros(npairs, bool)
+    for r0, r1 in res.rows:
+        mine |= (first >= r0) & (first < r1)
     sums = bucket_sums(jtarget, jexact, counts, m, np.nonzero(mine)[0])
     red = np.concatenate([sums.ravel(), [float(extra)]])
     if world > 1:
