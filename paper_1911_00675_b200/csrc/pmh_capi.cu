@@ -1497,7 +1497,8 @@ int pmh_probe_pipe_peak(int kind, double* gops_out, double* ms_out) {
 }
 
 int pmh_math_eval(int fn, const double* x, int64_t n, double* out, void* stream) {
-  if (fn < 0 || fn > 1 || n < 0) return set_error(PMH_ERR_INVALID, "fn must be 0 (log1p) or 1 (expm1)");
+  if (fn < 0 || fn > 2 || n < 0)
+    return set_error(PMH_ERR_INVALID, "fn must be 0 (log1p), 1 (expm1) or 2 (log1p, x = -U domain)");
   if (n == 0) return PMH_OK;
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;

@@ -143,7 +143,7 @@ __device__ __forceinline__ int64_t uniform_int(Stream& st, int64_t n) {  // K:11
 
 // E = -log1p(-U) given the 53 raw bits (K:120-122)
 __device__ __forceinline__ double exp1_from_bits(uint64_t b53) {
-  return -g_log1p(-((double)b53 * INV53));
+  return -g_log1p_negu(-((double)b53 * INV53));
 }
 
 // Conservative lower bound of fl(a * E(b53)) used ONLY to skip evaluating

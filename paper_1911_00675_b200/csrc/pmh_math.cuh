@@ -132,6 +132,70 @@ PMH_HD double g_log1p(double x) {
   return PMH_FMA(dk, PMH_LN2_HI, -((hfsq - (PMH_FMA(dk, PMH_LN2_LO, c) + t)) - f));
 }
 
+// g_log1p restricted to the SAMPLED domain x = -U, U = b 2^-53 in [0, 1)
+// (E = -log1p(-U), K:120-122): the same algorithm and roundings with the
+// branches that domain never takes removed, and the one it always takes
+// simplified:
+//   * x > -1, finite and non-positive: no NaN / inf / x >= 2^53 branches;
+//   * |x| > 0.2929 (k != 0): u = 1 + x is EXACT (x is a multiple of 2^-53
+//     and 0 < u < 0.71), so u - 1 == x exactly and glibc's correction
+//     c = x - (u - 1.0) (u < 1: k <= 0) is exactly +0 -- its division c / u
+//     (a full IEEE double division) is dropped;
+//   * the k = 0 and k != 0 results share one formula: with k = 0 and c = 0,
+//     fma(0, ln2_hi, -((hfsq - (fma(0, ln2_lo, 0) + t)) - f)) rounds exactly
+//     like f - (hfsq - t) (round-to-nearest is sign-symmetric, the result is
+//     never zero here), so the two argument reductions are selected and the
+//     polynomial runs once, without divergence.
+// Bit-identical to g_log1p (and glibc) on that domain: tests/native/
+// math_check.cpp (host) and tests/test_gpu_math.py (device) check it.
+PMH_HD double g_log1p_negu(double x) {
+  const int32_t hx = hi_word(x);
+  const int32_t ax = hx & 0x7fffffff;
+  if (ax < 0x3e200000) {           // |x| < 2^-29
+    if (ax < 0x3c900000) return x;
+    return PMH_FMA(-(x * x), 0.5, x);
+  }
+  // k != 0 reduction (u = 1 + x exact, c = 0)
+  const double u = 1.0 + x;
+  int32_t hu = hi_word(u);
+  int32_t k = (hu >> 20) - 1023;
+  hu &= 0x000fffff;
+  double un;
+  if (hu < 0x6a09e) {
+    un = with_hi_word(u, (uint32_t)hu | 0x3ff00000u);
+  } else {
+    k += 1;
+    un = with_hi_word(u, (uint32_t)hu | 0x3fe00000u);
+    hu = (0x00100000 - hu) >> 2;
+  }
+  double f = un - 1.0;
+  if (hx <= (int32_t)0xbfd2bec4) { k = 0; f = x; hu = 1; }   // |x| <= 0.2929: k = 0
+  const double hfsq = (f * 0.5) * f;
+  const double dk = (double)k;
+  if (hu == 0) {
+    if (f == 0.0) {
+      if (k == 0) return 0.0;
+      return PMH_FMA(dk, PMH_LN2_HI, PMH_FMA(dk, PMH_LN2_LO, 0.0));
+    }
+    const double R = PMH_FMA(-f, 0.66666666666666666, 1.0) * hfsq;
+    if (k == 0) return f - R;
+    return PMH_FMA(dk, PMH_LN2_HI, -((R - PMH_FMA(dk, PMH_LN2_LO, 0.0)) - f));
+  }
+  const double s = f / (2.0 + f);
+  const double z = s * s;
+  const double R2 = PMH_FMA(z, PMH_LP3, PMH_LP2);
+  const double R3 = PMH_FMA(z, PMH_LP5, PMH_LP4);
+  const double R4 = PMH_FMA(z, PMH_LP7, PMH_LP6);
+  const double z2 = z * z;
+  const double z4 = z2 * z2;
+  const double z6 = z2 * z4;
+  double R = PMH_FMA(z, PMH_LP1, z2 * R2);
+  R = PMH_FMA(z4, R3, R);
+  R = PMH_FMA(z6, R4, R);
+  const double t = (R + hfsq) * s;
+  return PMH_FMA(dk, PMH_LN2_HI, -((hfsq - (PMH_FMA(dk, PMH_LN2_LO, 0.0) + t)) - f));
+}
+
 // fdlibm constants (s_expm1.c)
 #define PMH_Q1 -3.33333333333331316428e-02 /* BFA11111 111110F4 */
 #define PMH_Q2 1.58730158725481460165e-03  /* 3F5A01A0 19FE5585 */

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256) point_probe_kernel(int iters, uint32_t* o
     const double U = (double)(wd & ((1ULL << 53) - 1ULL)) * INV53;
     const uint32_t lab = (uint32_t)(wd >> 53) & 1023u;
     if constexpr (KIND == 0) {
-      x = x + winv * -g_log1p(-U);
+      x = x + winv * -g_log1p_negu(-U);
     } else {
       x = winv * ((double)i - 1.0) + winv * (c1 * U);
     }
@@ -118,6 +118,8 @@ __global__ void math_eval_kernel(int fn, const double* __restrict__ x, int64_t n
        i += (int64_t)gridDim.x * blockDim.x) {
     if (fn == 0) {
       out[i] = g_log1p(x[i]);
+    } else if (fn == 2) {
+      out[i] = g_log1p_negu(x[i]);   // the sampled-domain specialisation (x = -U)
     } else {
       bool ok = true;
       const double e = g_expm1(x[i], &ok);

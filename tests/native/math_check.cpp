@@ -1,5 +1,5 @@
 // Host check: pmh_math.cuh (compiled by g++, -ffp-contract=off) vs glibc libm.
-// Usage: math_check <n_samples> ; prints "log1p_dom <mism> log1p_wide <mism>
+// Usage: math_check <n_samples> ; prints "log1p_dom <mism> log1p_negu <mism> log1p_wide <mism>
 // expm1 <mism> total <n>" and exits 0.
 #include <cmath>
 #include <cstdio>
@@ -14,7 +14,7 @@ static uint64_t mix64(uint64_t x) {
 
 int main(int argc, char** argv) {
   long n = argc > 1 ? atol(argv[1]) : 1000000;
-  long m_dom = 0, m_wide = 0, m_exp = 0, m_ok = 0;
+  long m_dom = 0, m_negu = 0, m_wide = 0, m_exp = 0, m_ok = 0;
   for (long i = 0; i < n; i++) {
     uint64_t w = mix64(0x1234ULL + (uint64_t)i * 0x9E3779B97F4A7C15ULL);
     uint64_t w2 = mix64(0x777ULL + (uint64_t)i * 0x9E3779B97F4A7C15ULL);
@@ -25,6 +25,7 @@ int main(int argc, char** argv) {
     if ((i & 7) == 2) k = (1ULL << 53) - 1 - (k >> (w2 & 63));
     double x = -((double)k * 1.1102230246251565e-16);
     if (pmh::dbl_bits(pmh::g_log1p(x)) != pmh::dbl_bits(log1p(x))) m_dom++;
+    if (pmh::dbl_bits(pmh::g_log1p_negu(x)) != pmh::dbl_bits(log1p(x))) m_negu++;
     // wide: any finite double > -1
     double y = pmh::bits_dbl(w2 & 0x7fefffffffffffffULL);
     if (w & 1) y = -(double)(w2 >> 11) * 1.1102230246251565e-16 * ((w >> 1) & 1 ? 1.0 : 0.5);
@@ -41,7 +42,7 @@ int main(int argc, char** argv) {
     if (!ok) m_ok++;
     else if (pmh::dbl_bits(e) != pmh::dbl_bits(expm1(arg))) m_exp++;
   }
-  printf("log1p_dom %ld log1p_wide %ld expm1 %ld expm1_outofrange %ld total %ld\n",
-         m_dom, m_wide, m_exp, m_ok, n);
+  printf("log1p_dom %ld log1p_negu %ld log1p_wide %ld expm1 %ld expm1_outofrange %ld total %ld\n",
+         m_dom, m_negu, m_wide, m_exp, m_ok, n);
   return 0;
 }

@@ -80,6 +80,18 @@ def test_device_log1p_bit_exact_vs_glibc(glibc):
     assert frac == 0.0
 
 
+def test_device_log1p_sampled_domain_specialisation_bit_exact(glibc):
+    """g_log1p_negu -- the log1p every kernel calls (E = -log1p(-U)) -- on the
+    device, against the host glibc, bit for bit."""
+    x = _log1p_inputs()
+    got = _device(2, x).view(np.uint64)
+    ref = _host(glibc.glibc_log1p, x).view(np.uint64)
+    frac = float((got != ref).mean())
+    print(f"device log1p (x = -U specialisation) vs glibc: {int((got != ref).sum())} "
+          f"mismatches in {x.size} (fraction {frac:.3g})")
+    assert frac == 0.0
+
+
 def test_device_expm1_bit_exact_vs_glibc(glibc):
     x = _expm1_inputs()
     got = _device(1, x)
