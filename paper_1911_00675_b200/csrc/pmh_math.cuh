@@ -148,6 +148,19 @@ PMH_HD double g_log1p(double x) {
 //     polynomial runs once, without divergence.
 // Bit-identical to g_log1p (and glibc) on that domain: tests/native/
 // math_check.cpp (host) and tests/test_gpu_math.py (device) check it.
+// Device: the polynomial and ln2 constants come from the constant bank (an
+// FP64 instruction reads a c[][] operand directly; full 64-bit literals would
+// be rebuilt in registers by two moves each, every point).
+#if defined(__CUDACC__)
+__constant__ double g_log1p_k[9] = {PMH_LP1, PMH_LP2, PMH_LP3, PMH_LP4, PMH_LP5, PMH_LP6,
+                                    PMH_LP7, PMH_LN2_HI, PMH_LN2_LO};
+#endif
+#if defined(__CUDA_ARCH__)
+#define PMH_KC(i, lit) g_log1p_k[i]
+#else
+#define PMH_KC(i, lit) (lit)
+#endif
+
 PMH_HD double g_log1p_negu(double x) {
   const int32_t hx = hi_word(x);
   const int32_t ax = hx & 0x7fffffff;
@@ -175,25 +188,25 @@ PMH_HD double g_log1p_negu(double x) {
   if (hu == 0) {
     if (f == 0.0) {
       if (k == 0) return 0.0;
-      return PMH_FMA(dk, PMH_LN2_HI, PMH_FMA(dk, PMH_LN2_LO, 0.0));
+      return PMH_FMA(dk, PMH_KC(7, PMH_LN2_HI), PMH_FMA(dk, PMH_KC(8, PMH_LN2_LO), 0.0));
     }
     const double R = PMH_FMA(-f, 0.66666666666666666, 1.0) * hfsq;
     if (k == 0) return f - R;
-    return PMH_FMA(dk, PMH_LN2_HI, -((R - PMH_FMA(dk, PMH_LN2_LO, 0.0)) - f));
+    return PMH_FMA(dk, PMH_KC(7, PMH_LN2_HI), -((R - PMH_FMA(dk, PMH_KC(8, PMH_LN2_LO), 0.0)) - f));
   }
   const double s = f / (2.0 + f);
   const double z = s * s;
-  const double R2 = PMH_FMA(z, PMH_LP3, PMH_LP2);
-  const double R3 = PMH_FMA(z, PMH_LP5, PMH_LP4);
-  const double R4 = PMH_FMA(z, PMH_LP7, PMH_LP6);
+  const double R2 = PMH_FMA(z, PMH_KC(2, PMH_LP3), PMH_KC(1, PMH_LP2));
+  const double R3 = PMH_FMA(z, PMH_KC(4, PMH_LP5), PMH_KC(3, PMH_LP4));
+  const double R4 = PMH_FMA(z, PMH_KC(6, PMH_LP7), PMH_KC(5, PMH_LP6));
   const double z2 = z * z;
   const double z4 = z2 * z2;
   const double z6 = z2 * z4;
-  double R = PMH_FMA(z, PMH_LP1, z2 * R2);
+  double R = PMH_FMA(z, PMH_KC(0, PMH_LP1), z2 * R2);
   R = PMH_FMA(z4, R3, R);
   R = PMH_FMA(z6, R4, R);
   const double t = (R + hfsq) * s;
-  return PMH_FMA(dk, PMH_LN2_HI, -((hfsq - (PMH_FMA(dk, PMH_LN2_LO, 0.0) + t)) - f));
+  return PMH_FMA(dk, PMH_KC(7, PMH_LN2_HI), -((hfsq - (PMH_FMA(dk, PMH_KC(8, PMH_LN2_LO), 0.0) + t)) - f));
 }
 
 // fdlibm constants (s_expm1.c)
