@@ -85,8 +85,8 @@ POINT_KIND = {"probminhash1": 0, "probminhash1a": 0, "probminhash2": 0,
               "probminhash3": 1, "probminhash3a": 1, "probminhash4": 1}
 # c_v of SURVEY.md §8d: SASS instructions (issue slots) per point of the
 # per-point probe's loop body, by point kind (tools/sass_loop_cost.py ->
-# profiles/r02_point_cost_sass.txt): a log1p point 270, a TruncExp point 81
-C_V = {0: 270, 1: 81}
+# profiles/r02b_point_cost_sass.txt): a log1p point 183, a TruncExp point 81
+C_V = {0: 183, 1: 81}
 
 
 def _peaks():
@@ -655,6 +655,9 @@ def run_config5(args, ctx):
 
 
 def main():
+    # stdout carries exactly one JSON line: NCCL's own banner (NCCL_DEBUG set
+    # on the box) goes to stderr
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
