@@ -278,9 +278,10 @@ int pmh_probe_pipe_peak(int kind, double* gops_out, double* ms_out);
  * per-variant roofline divides by.  Synchronous. */
 int pmh_probe_point_rate(int kind, double* gpts_out, double* ms_out);
 
-/* The device build of the glibc log1p (fn 0) / expm1 (fn 1) restatements the
- * kernels use (csrc/pmh_math.cuh; reference K:120-122, K:146), evaluated on n
- * DEVICE doubles x into out (expm1: NaN where it reports no result).
+/* The device build of the glibc log1p (fn 0) / expm1 (fn 1) restatements
+ * (csrc/pmh_math.cuh; reference K:120-122, K:146), and (fn 2) the log1p
+ * specialised to the sampled domain x = -U that the kernels call, evaluated on
+ * n DEVICE doubles x into out (expm1: NaN where it reports no result).
  * Stream-ordered.  For parity tests of the transcendental itself. */
 int pmh_math_eval(int fn, const double* x, int64_t n, double* out, void* stream);
 
