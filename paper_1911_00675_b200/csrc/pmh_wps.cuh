@@ -32,6 +32,9 @@ constexpr int WPS_MMAX = 64;
 #endif
 constexpr int WPS_NMAX = PMH_WPS_NMAX;   // largest set the warp-per-set kernel takes
 constexpr int WPS_THREADS = 128;
+#ifndef PMH_WPS_HEAVY_FIRST
+#define PMH_WPS_HEAVY_FIRST 1
+#endif
 #ifndef PMH_WPS_MINB
 #define PMH_WPS_MINB 6   // CTAs per SM the register budget allows (80 registers)
 #endif
@@ -59,6 +62,7 @@ struct WpsWarp {
   uint64_t ids[2][WPS_NMAX];
   double w[2][WPS_NMAX];
   uint8_t fy[WPS_MMAX][32];   // [p][lane]
+  uint8_t ord[WPS_NMAX];      // processing order of the set's elements (heaviest first)
 };
 
 __host__ __device__ inline bool wps_eligible(int family, int64_t m) {
@@ -151,6 +155,46 @@ __global__ void __launch_bounds__(WPS_THREADS, PMH_WPS_MINB) sketch_wps_kernel(S
     double tg = (double)m * (lnm + a.tconst) / W;
     if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
     bool failed = false;
+    // Heaviest first (longest-processing-time order): an element's point
+    // count is ~ t w (at most m without replacement), so with skewed weights
+    // (configs[3]: Pareto 1.5) a heavy element taken last leaves its lane
+    // running alone while the other lanes idle at the end of the set.  A
+    // counting sort on floor(log2(1 + t w)) (8 buckets, descending) orders
+    // the lanes' refill; element indices (the tie-break) are unchanged.
+    if (weighted && PMH_WPS_HEAVY_FIRST) {
+      int key[WPS_NMAX / 32];
+      int base[8];
+#pragma unroll
+      for (int r = 0; r < WPS_NMAX / 32; r++) {
+        const int64_t e = lane + 32 * r;
+        key[r] = -1;
+        if (e < n) {
+          const double pts = tg * w[e];
+          const int k = pts < 1.0 ? 0 : 1 + ilogb(pts);
+          key[r] = k > 7 ? 7 : k;
+        }
+      }
+      const unsigned lt = (1u << lane) - 1u;
+      int run = 0;
+#pragma unroll
+      for (int b = 7; b >= 0; b--) {
+        base[b] = run;
+#pragma unroll
+        for (int r = 0; r < WPS_NMAX / 32; r++) run += __popc(__ballot_sync(0xffffffffu, key[r] == b));
+      }
+#pragma unroll
+      for (int r = 0; r < WPS_NMAX / 32; r++) {
+#pragma unroll
+        for (int b = 7; b >= 0; b--) {
+          const unsigned mk = __ballot_sync(0xffffffffu, key[r] == b);
+          if (key[r] == b) ws->ord[base[b] + __popc(mk & lt)] = (uint8_t)(lane + 32 * r);
+          base[b] += __popc(mk);
+        }
+      }
+    } else {
+      for (int64_t e = lane; e < n; e += 32) ws->ord[e] = (uint8_t)e;
+    }
+    __syncwarp();
     LaneElT<LaneDenseFY> st;
     st.fy.col = &ws->fy[0][lane];
     st.e = 0;
@@ -168,7 +212,7 @@ __global__ void __launch_bounds__(WPS_THREADS, PMH_WPS_MINB) sketch_wps_kernel(S
           const int take = n - next < idle ? (int)(n - next) : idle;
           const int rank = __popc(~am & lt);
           if (!act && rank < take) {
-            const int32_t e = (int32_t)(next + rank);
+            const int32_t e = (int32_t)ws->ord[next + rank];
             const double winv = weighted ? 1.0 / w[e] : 1.0;
             act = lane_init<F>(c, T, st, e, ids[e], winv, ctx_thr(c));
           }
