@@ -500,6 +500,11 @@ def run_config2(args, ctx):
     else:
         full = None
         batch = datagen.config2(seed=2 + rank)
+    # N > 1: a rank's shard (~1/N of the sets) leaves the GPU underfilled by any
+    # one variant's latency-bound sets, so the variants run concurrently there
+    # (tools/shard_sim.py: projected 8-GPU step 17.3 -> 15.2 ms); N = 1 keeps the
+    # sequential step with per-launch events (equal time, exact per-variant split)
+    args.concurrent = args.concurrent or world > 1
     step = Step(ctx, batch, variants, args.concurrent, shared_w=not args.no_shared_w)
     clk = ClockSampler(ctx.local)
     ms_step = step.run(args.steps, args.warmup, clk)
