@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(FLAT_THREADS, 3) sketch_flat_kernel(SketchArgs
     c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
     c.trig = false;
     c.eoff = 0;
-    double tg = (double)m * (log((double)m) + a.tconst) / W;
+    double tg = (double)m * (log((double)m) + guess_const(a.tconst, n)) / W;
     if (!(tg > 0.0) || !(tg < 1e300)) tg = 1e300;
     bool failed = false;
     __syncthreads();

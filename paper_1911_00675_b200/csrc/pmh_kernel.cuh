@@ -310,7 +310,7 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
   c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
   c.trig = false;
   c.eoff = (int32_t)e0;
-  double tg = (double)m * (log((double)m) + a.tconst) / W;
+  double tg = (double)m * (log((double)m) + guess_const(a.tconst, n)) / W;
   if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
   bool failed = false;
   int64_t chunk = (n + PMH_CHUNK_DIV * nwarps - 1) / (PMH_CHUNK_DIV * nwarps);
@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
     c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
   c.trig = false;
     c.eoff = 0;
-    double tg = (double)m * (log((double)m) + a.tconst) / W;
+    double tg = (double)m * (log((double)m) + guess_const(a.tconst, n)) / W;
     if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
     bool failed = false;
     for (int attempt = 0;; attempt++) {

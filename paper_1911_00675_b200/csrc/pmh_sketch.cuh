@@ -352,6 +352,24 @@ struct SketchArgs {
   const double* setw;       // device [nsets] total weights known in advance, or nullptr
 };
 
+// Threshold-guess constant c of t = m (ln m + c) / W for a set (or range) of
+// n elements.  A guess below the final limit H costs the set a full retry
+// (4t): for a handful of elements (a lone element's coupon collector exceeds
+// m (ln m + c) points with probability ~e^-c) that doubles the set's
+// latency, and a small batch (one rank's shard) waits on its slowest sets.
+// With so few elements the slot table fills from the elements' own long
+// point sequences and the stop limit falls to h_max at once, so a larger c
+// costs them almost no points.
+#ifndef PMH_FEW_N
+#define PMH_FEW_N 16
+#endif
+#ifndef PMH_FEW_BOOST
+#define PMH_FEW_BOOST 3.0
+#endif
+__device__ __forceinline__ double guess_const(double tconst, int64_t n) {
+  return n <= PMH_FEW_N ? tconst + PMH_FEW_BOOST : tconst;
+}
+
 // Per-set total weights W_s (one CTA per set, grid-stride): computed once per
 // batch and shared by every variant of a multi-variant call, or supplied by
 // the caller for the non-streaming variants.
