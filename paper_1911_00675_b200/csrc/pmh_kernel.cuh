@@ -474,14 +474,19 @@ namespace pmh {
 // per-set barriers dominate, so they all run warp-per-set.
 // ---------------------------------------------------------------------------
 #ifndef PMH_SMALL_N
-#define PMH_SMALL_N 3
+#define PMH_SMALL_N 1
 #endif
 #ifndef PMH_SMALL_N_STATIC
 #define PMH_SMALL_N_STATIC 7
 #endif
 // sets up to this size run warp-per-set at large m (measured on configs[1]:
 // cutoff 7 vs 3 is 2% / 6% faster for ProbMinHash 1 / 3 and 4% slower for
-// the Fisher-Yates families 2 / 4, whose warp-per-set map costs more)
+// the Fisher-Yates families 2 / 4, whose warp-per-set map costs more).  The
+// Fisher-Yates families send only singletons there: a warp runs a set's long
+// elements one after another, and 2-3 elements of ~m points each made those
+// sets the latency floor of a small batch (1/8 shard of configs[1]: the
+// n < 4 class 0.89 -> 0.38 ms for ProbMinHash2, 0.53 -> 0.25 for 4; the
+// whole batch unchanged)
 constexpr int64_t SMALL_N = PMH_SMALL_N;
 constexpr int64_t SMALL_N_STATIC = PMH_SMALL_N_STATIC;
 #ifndef PMH_SMALL_N_SMALLM
