@@ -57,6 +57,9 @@ __device__ __forceinline__ void slot_offer_global(Slot* p, unsigned long long h,
   }
 }
 
+#ifndef PMH_SPLIT_SMALL_FAIR
+#define PMH_SPLIT_SMALL_FAIR 65536
+#endif
 // single CTA: which sets are split, the parts per set, their prefix
 __global__ void split_prep_kernel(SplitArgs a, long long cta_slots) {
   __shared__ long long s_run;
@@ -66,7 +69,12 @@ __global__ void split_prep_kernel(SplitArgs a, long long cta_slots) {
     // threshold: the largest power of two not above the fair share (total
     // cost / CTA slots), but at least the smallest power of two >= one part
     const long long total = (a.offsets[a.nsets] - a.offsets[0]) + a.c_off * a.nsets;
-    const long long fair = total / (cta_slots > 0 ? cta_slots : 1);
+    long long fair = total / (cta_slots > 0 ? cta_slots : 1);
+    // a small batch (one rank's shard): a quarter of the fair share, so the
+    // LPT tail is a few short parts instead of one unsplit set near the
+    // fair share (large batches keep whole sets: a part prunes with its own
+    // minima only, so splitting costs work there)
+    if (fair < PMH_SPLIT_SMALL_FAIR) fair /= 4;
     long long floor_p2 = 1;
     while (floor_p2 < a.split_n + a.c_off) floor_p2 <<= 1;
     long long p2 = floor_p2;
