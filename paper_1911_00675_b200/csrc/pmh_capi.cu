@@ -520,6 +520,7 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
 // per-set total weights into a stream-ordered pool buffer (nullptr on error)
 static double* set_weights_tmp(const double* weights, const int64_t* offsets, int64_t nsets,
                                cudaStream_t st) {
+  ensure_pool_retained();
   double* d = nullptr;
   if (cudaMallocAsync((void**)&d, sizeof(double) * (size_t)nsets, st) != cudaSuccess) return nullptr;
   int64_t grid = nsets < 148 * 16 ? nsets : 148 * 16;
@@ -567,6 +568,7 @@ int pmh_sketch_csr_multi_async(const int* algos, int nalgos, int64_t m, const ui
   cudaStream_t st = (cudaStream_t)stream;
   if (nalgos < 1 || nalgos > 32 || !algos || !sig_outs)
     return set_error(PMH_ERR_INVALID, "1..32 algorithms with outputs required");
+  ensure_pool_retained();
   for (int k = 0; k < nalgos; k++) {
     int vrc = validate_sketch(algos[k], m, weights, nsets);
     if (vrc != PMH_OK) return vrc;
@@ -612,6 +614,11 @@ static int sketch_async_impl(int algo, int64_t m, const uint64_t* ids, const dou
                              const int64_t* offsets, int64_t nsets, uint64_t* sig_out,
                              int64_t* stats_out, int64_t* d_status, cudaStream_t st,
                              int aux_slot, const double* setw) {
+  // the stream-ordered workspaces of the call (set order, split tables) must
+  // stay mapped between calls: with the pool's default release threshold 0
+  // they are unmapped at every synchronisation and re-mapped by the next
+  // call, a host-side stall of up to ~40 ms before its first kernel
+  ensure_pool_retained();
   const int fam = family_of(algo);
   int vrc = validate_sketch(algo, m, weights, nsets);
   if (vrc != PMH_OK) return vrc;
@@ -1162,6 +1169,7 @@ int launch_allpairs_reduce(const uint64_t* rows, int64_t len, int64_t m, Cmp cmp
 int launch_allpairs_exact2(const uint64_t* sigs, int64_t m, int64_t r0, int64_t r1, int64_t c0,
                            int64_t c1, int32_t thr, uint64_t* hist, uint64_t* pairs, int64_t cap,
                            uint64_t* cursor, cudaStream_t st) {
+  ensure_pool_retained();
   const int64_t rows = r1 - r0, cols = c1 - c0;
   int64_t ccap = rows * cols;                 // upper bound on the range's pairs
   if (ccap > (1LL << 22)) ccap = 1LL << 22;
@@ -1222,6 +1230,7 @@ __global__ void join_map_init_kernel(PairSlot* map, int64_t slots) {
 int pmh_allpairs_join_hist(const uint64_t* sigs, int64_t n, int64_t m, int64_t r0, int64_t r1,
                            int64_t c0, int64_t c1, int32_t thr, uint64_t* hist, uint64_t* pairs,
                            int64_t cap, uint64_t* cursor, int64_t max_visits, void* stream) {
+  ensure_pool_retained();
   if (m < 1 || m > 65535 || r0 < 0 || r1 > n || c0 < 0 || c1 > n || r0 > r1 || c0 > c1)
     return set_error(PMH_ERR_INVALID, "bad tile bounds");
   if (n >= (1LL << 31)) return set_error(PMH_ERR_INVALID, "n must be < 2^31");
