@@ -450,3 +450,22 @@ def test_host_multi_async_pipelined_batches():
         ref, _ = sketch_csr_multi(algos, 128, b.ids, b.weights, b.offsets)
         for got, r in zip(o, ref):
             assert np.array_equal(got.numpy().view(np.uint64), r)
+
+
+def test_config2_shards_equal_full_batch():
+    """The strong-scaling split (dist.shard_ranges_multi, what bench.py --gpus 8
+    gives each rank) is exact: every shard computed alone equals its rows of
+    the full configs[1] batch.  A shard is a small batch, so this also runs
+    the small-batch split rule (sets cut at a quarter of the fair share) and
+    the singleton-only warp-per-set path against the whole-batch schedule."""
+    from paper_1911_00675_b200.dist import local_batch, shard_ranges_multi
+    full = datagen.config2()
+    variants = ["pminhash", "probminhash1", "probminhash2", "probminhash3", "probminhash4"]
+    shards = shard_ranges_multi(full.offsets, 8, 1024, variants)
+    ids, w, off = _dev(full)
+    for algo in variants:
+        whole = sigs_to_numpy(sketch_batch(algo, ids, w, off, 1024)[0])
+        for s0, s1 in shards:
+            b = local_batch(full, (s0, s1))
+            part = sigs_to_numpy(sketch_batch(algo, *_dev(b), 1024)[0])
+            assert np.array_equal(part, whole[s0:s1]), (algo, s0, s1)
