@@ -16,6 +16,11 @@
  * Algorithm ids are the reference's ALG_* constants (K:866-881).
  * Return value: PMH_OK or a negative PMH_ERR_* code; *err_set (if non-NULL)
  * receives the index of the first offending set for EMPTY / RANDOMNESS.
+ * Workspaces are stream-ordered allocations from the device's DEFAULT memory
+ * pool; the first allocating call sets that pool's release threshold to
+ * UINT64_MAX, so freed workspaces stay mapped for the next call instead of
+ * being unmapped at every synchronisation (a caller sharing the default pool
+ * keeps its freed memory cached too; cudaMemPoolTrimTo releases it).
  */
 #ifndef PMH_H_
 #define PMH_H_
