@@ -24,6 +24,22 @@ namespace pmh {
 #define PMH_HEAVY_POINTS 16.0   // measured best on config 2 (4 / 6 / 8 / 12 / 16 / 24 / 32 / 48 tried)
 #endif
 constexpr double HEAVY_POINTS = PMH_HEAVY_POINTS;   // expected points above which mode B runs
+// Sets that fill every lane of the CTA (n >= 256) with elements of EQUAL
+// weight (the unweighted families) run lane-per-element up to a much longer
+// sequence: their lanes stay in step (point counts differ only by the points'
+// own randomness), while a warp-cooperative element of 36 points (configs[2]:
+// m = 4096, n = 1000) fills 36 of 64 lane slots (unweighted 1 there: 139 ->
+// 84 ms).  Below 256 elements the lanes are too few and the warp path wins
+// (measured at n = 32 ... 8192, tools/uw_sweep.py).
+#ifndef PMH_HEAVY_POINTS_UW
+#define PMH_HEAVY_POINTS_UW 256
+#endif
+#ifndef PMH_HEAVY_UW_MIN_N
+#define PMH_HEAVY_UW_MIN_N 256
+#endif
+#ifndef PMH_HEAVY_POINTS_BIGN
+#define PMH_HEAVY_POINTS_BIGN PMH_HEAVY_POINTS
+#endif
 
 
 // Division-free prefilter for the common case of large sets: decide from the
@@ -68,17 +84,12 @@ constexpr int SKETCH_THREADS = 256;
 // static __shared__ state too (SetShared and friends, < 1 KB)
 constexpr size_t SMEM_DYN_MAX = 227 * 1024 - 1024;
 
-// bytes of one warp's dense Fisher-Yates map (16-byte multiple)
-__host__ __device__ inline size_t fy_map_bytes(int64_t m, bool fy16) {
-  return ((fy16 ? 2 : 4) * (size_t)(m + 1) + 15) & ~(size_t)15;
-}
-
 __host__ __device__ inline size_t sketch_smem_bytes(int family, int64_t m, int threads,
                                                     bool fy16 = false) {
   const int nw = threads / 32;
   size_t b = sizeof(Slot) * (size_t)m;
   b += sizeof(WarpScratch) * (size_t)nw;
-  if (family_uses_fy(family)) b += fy_map_bytes(m, fy16) * (size_t)nw;
+  if (family_uses_fy(family)) b += fy_region_bytes(m, fy16) * (size_t)nw;
   return (b + 15) & ~(size_t)15;
 }
 
@@ -96,6 +107,21 @@ constexpr int SKETCH_THREADS_BIG = 512;
 __host__ __device__ inline bool sketch_use_big(int family, int64_t m) {
   return family_uses_fy(family) && m > 2048 && m < 8192 &&
          sketch_smem_bytes(family, m, SKETCH_THREADS_BIG, true) <= SMEM_DYN_MAX;
+}
+
+// Expected points of an element above which it runs warp-cooperatively, for
+// a set of n elements in the CTA kernels.  The Fisher-Yates families stay
+// within what a lane's hash map holds.
+template <int F, bool FY16>
+__device__ __forceinline__ int32_t heavy_points_for(bool weighted, int64_t n, int64_t m) {
+  double h = HEAVY_POINTS;
+  if (n >= PMH_HEAVY_UW_MIN_N) h = weighted ? (double)PMH_HEAVY_POINTS_BIGN : (double)PMH_HEAVY_POINTS_UW;
+  if constexpr (family_uses_fy(F)) {
+    const uint32_t s = hashfy_slots(fy_region_bytes(m, FY16));
+    const double cap = (double)(s - (s >> 3)) - 4.0;   // HashFY::room less a margin
+    if (h > cap) h = cap;
+  }
+  return (int32_t)h;
 }
 
 // Per-warp element loop shared by the CTA-per-set and warp-per-set kernels:
@@ -128,7 +154,7 @@ struct LocalGrab {
 // of line so the register budget of the heavy recurrences does not spill the
 // streaming prefilter loop around it (one call per batch, i.e. per ~4-32
 // prefilter iterations).  Returns true if an element hit a loop cap.
-template <int F, bool FY16>
+template <int F, bool FY16, bool HASHFY>
 __device__ __forceinline__ bool run_batch(SetCtx& c, const Tables& T, const uint64_t* ids,
                                        const double* w, WarpScratch* wscr, uint32_t* fy_dense,
                                        bool warp_ok, int lane, int take, int qn) {
@@ -143,11 +169,20 @@ __device__ __forceinline__ bool run_batch(SetCtx& c, const Tables& T, const uint
     const uint64_t id = __ldg(&ids[e]);
     double winv = 1.0;
     if (family_weighted(F) && w) winv = 1.0 / __ldg(&w[e]);
-    heavy = warp_ok && ctx_thr(c) > HEAVY_POINTS * winv;
+    heavy = warp_ok && ctx_thr(c) > (double)c.heavy_pts * winv;
     if (!heavy) {
-      SparseFY fy; fy.reset();
-      status = run_element<F>(c, T, fy, e, id, winv);
+      if constexpr (HASHFY && family_uses_fy(F)) {
+        HashFY fy; fy.reset(fy_dense, lane, hashfy_slots(fy_region_bytes(c.m, FY16)));
+        status = run_element<F>(c, T, fy, e, id, winv);
+      } else {
+        SparseFY fy; fy.reset();
+        status = run_element<F>(c, T, fy, e, id, winv);
+      }
     }
+  }
+  if constexpr (HASHFY && family_uses_fy(F)) {
+    if (lane == 0) wscr->fy_dirty = 1u;
+    __syncwarp();
   }
   if (status == EL_FAIL) failed = true;
   unsigned hm = __ballot_sync(0xffffffffu, act && (heavy || status == EL_NEED_WARP));
@@ -190,7 +225,7 @@ __device__ __forceinline__ bool run_batch(SetCtx& c, const Tables& T, const uint
 // register prefetch is kept across the heavy batch.  32-bit element indices
 // (sets hold < 2^31 elements); rejections counted in a register (stats only).
 // (PMH_EPL is defined in pmh_warp.cuh next to the queue it sizes)
-template <int F, bool FY16, class Grab>
+template <int F, bool FY16, bool HASHFY, class Grab>
 __device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const uint64_t* ids,
                                            const double* w, int64_t n, int64_t chunk, Grab& grab,
                                            WarpScratch* wscr, uint32_t* fy_dense, bool warp_ok,
@@ -230,7 +265,7 @@ __device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const 
     }
     while (qn >= 32 || (!more && qn > 0)) {
       const int take = qn < 32 ? qn : 32;
-      if (run_batch<F, FY16>(c, T, ids, w, wscr, fy_dense, warp_ok, lane, take, qn)) failed = true;
+      if (run_batch<F, FY16, HASHFY>(c, T, ids, w, wscr, fy_dense, warp_ok, lane, take, qn)) failed = true;
       qn -= take;
       __syncwarp();
     }
@@ -310,6 +345,7 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
   c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
   c.trig = false;
   c.eoff = (int32_t)e0;
+  c.heavy_pts = heavy_points_for<F, FY16>(w != nullptr, n, m);
   double tg = (double)m * (log((double)m) + guess_const(a.tconst, n)) / W;
   if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
   bool failed = false;
@@ -321,7 +357,7 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
     if (threadIdx.x == 0) sh.next = 0;
     __syncthreads();
     SharedGrab grab{&sh.next, (unsigned)chunk};
-    warp_elements<F, FY16>(c, a.T, ids, w, n, chunk, grab, wscr, fy_dense, warp_ok, failed, lane);
+    warp_elements<F, FY16, true>(c, a.T, ids, w, n, chunk, grab, wscr, fy_dense, warp_ok, failed, lane);
     __syncthreads();
     // verification: every slot non-empty and <= tguess
     unsigned long long mx = 0;
@@ -364,10 +400,10 @@ __device__ __forceinline__ void sketch_cta_setup(unsigned char* smem, int64_t m,
   *slots = reinterpret_cast<Slot*>(smem);
   *wscr = reinterpret_cast<WarpScratch*>(smem + sizeof(Slot) * m) + wid;
   *fy_dense = reinterpret_cast<uint32_t*>(smem + sizeof(Slot) * m + sizeof(WarpScratch) * nwarps +
-                                          fy_map_bytes(m, FY16) * (size_t)wid);
+                                          fy_region_bytes(m, FY16) * (size_t)wid);
   if (family_uses_fy(F)) {  // epoch 0 never matches: the map starts empty
     fy_clear<FY16>(*fy_dense, m, lane);
-    if (lane == 0) (*wscr)->epoch = 0;
+    if (lane == 0) { (*wscr)->epoch = 0; (*wscr)->fy_dirty = 0u; }
   }
 }
 
@@ -526,7 +562,7 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
                                              sizeof(WarpSetVars));
   if (family_uses_fy(F)) {
     for (int64_t p = lane; p <= m; p += 32) fy[p] = 0;
-    if (lane == 0) ws->epoch = 0;
+    if (lane == 0) { ws->epoch = 0; ws->fy_dirty = 0u; }
   }
   const int64_t n_large = (int64_t)a.counts[0];
   const int64_t n_small = a.nsets - n_large;
@@ -563,13 +599,14 @@ __global__ void __launch_bounds__(128) sketch_small_kernel(SketchArgs a) {
     c.points = 0; c.updates = 0; c.multi = 0; c.tprev = -1.0; c.since_refresh = 0;
   c.trig = false;
     c.eoff = 0;
+    c.heavy_pts = (int32_t)HEAVY_POINTS;
     double tg = (double)m * (log((double)m) + guess_const(a.tconst, n)) / W;
     if (!(tg > 0.0)) tg = __longlong_as_double(0x7FF0000000000000LL);
     bool failed = false;
     for (int attempt = 0;; attempt++) {
       c.tguess = tg;
       LocalGrab grab{0u, 32u * PMH_EPL};
-      warp_elements<F, false>(c, a.T, ids, w, n, 32 * PMH_EPL, grab, ws, fy, warp_ok, failed, lane);
+      warp_elements<F, false, false>(c, a.T, ids, w, n, 32 * PMH_EPL, grab, ws, fy, warp_ok, failed, lane);
       unsigned long long mx = 0;
       for (int64_t k = lane; k < m; k += 32) {
         const unsigned long long h = slots[k].h;

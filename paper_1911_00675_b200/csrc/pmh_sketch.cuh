@@ -58,6 +58,7 @@ struct SetCtx {
   bool trig;                         // this lane lowered the maximum slot / filled the last
                                      // one: the warp refreshes h_max after the batch
   int32_t eoff;                      // in-set index of element 0 (a split set's part)
+  int32_t heavy_pts;                 // expected points above which an element runs warp-cooperatively
 };
 
 __device__ __forceinline__ double ctx_thr(const SetCtx& c) {

@@ -42,7 +42,7 @@ struct WarpScratch {
   uint32_t flags;       // bit0: batch ended by a slow path; bit1: fail
   uint64_t next_off;    // absolute bit offset after the batch
   uint32_t epoch;       // Fisher-Yates map epoch (one per warp-processed element)
-  uint32_t pad;
+  uint32_t fy_dirty;    // the map region last held the lanes' hash maps (HashFY): clear before use
   uint32_t gm[32];      // parallel Fisher-Yates: lanes whose target is i0 + k
   int32_t sq[SQ_CAP];   // survivor queue of the large-set path (element indices, LIFO)
 };
@@ -74,6 +74,18 @@ struct EpochFY {
   }
 };
 
+// bytes of one warp's dense Fisher-Yates map (16-byte multiple)
+__host__ __device__ inline size_t fy_map_bytes(int64_t m, bool fy16) {
+  return ((fy16 ? 2 : 4) * (size_t)(m + 1) + 15) & ~(size_t)15;
+}
+// bytes of one warp's map REGION in the CTA kernels: the dense map or the
+// lanes' hash maps (HashFY below; at least 32 slots per lane), whichever is larger
+constexpr size_t HASHFY_MIN_BYTES = 32 * 128;
+__host__ __device__ inline size_t fy_region_bytes(int64_t m, bool fy16) {
+  const size_t d = fy_map_bytes(m, fy16);
+  return d > HASHFY_MIN_BYTES ? d : HASHFY_MIN_BYTES;
+}
+
 // clear a dense map (entries 0..m) -- epoch 0 never matches
 template <bool H16>
 __device__ __forceinline__ void fy_clear(uint32_t* fy, int64_t m, int lane) {
@@ -83,6 +95,71 @@ __device__ __forceinline__ void fy_clear(uint32_t* fy, int64_t m, int lane) {
   } else {
     for (int64_t p = lane; p <= m; p += 32) fy[p] = 0;
   }
+}
+
+// Per-LANE lazy Fisher-Yates maps for the lane-per-element path, in the SAME
+// shared-memory region as the warp's dense map (a warp runs its lanes'
+// elements first, then the batch's warp-cooperative ones; WarpScratch.fy_dirty
+// tells warp_el_fy to clear the region before the dense map uses it again).
+// Lane l owns words l, l + 32, l + 64, ... (its own bank: conflict-free), an
+// open-addressing table of S = 2^k <= 64 slots, entry = pos << 16 | value
+// (m < 65536), linear probing from pos & (S - 1); which slots are in use is a
+// 64-bit register mask, so a new element starts with an O(1) reset.  The
+// register-resident SparseFY it replaces held 16 entries in 32 registers and
+// scanned all of them per step.
+struct HashFY {
+  uint32_t* a;        // region + lane
+  uint64_t used;
+  uint32_t mask;      // S - 1
+  uint32_t room;      // entries left before the element goes to the warp path
+  __device__ __forceinline__ void reset(uint32_t* region, int lane, uint32_t slots) {
+    a = region + lane;
+    used = 0ULL;
+    mask = slots - 1u;
+    room = slots - (slots >> 3);   // load factor <= 7/8
+  }
+  // one lazy Fisher-Yates step (K:222-235): returns perm[j] and sets
+  // perm[j] = perm[i] (both read before the write); 0 when the table is full
+  __device__ __forceinline__ int32_t swap_step(int32_t i, int32_t j) {
+    int32_t vj = j, vi = i;
+    uint32_t s = (uint32_t)j & mask;
+    bool found = false;
+    while ((used >> s) & 1ULL) {
+      const uint32_t en = a[s << 5];
+      if ((en >> 16) == (uint32_t)j) { vj = (int32_t)(en & 0xffffu); found = true; break; }
+      s = (s + 1u) & mask;
+    }
+    if (i == j) {
+      vi = vj;
+    } else {
+      uint32_t t = (uint32_t)i & mask;
+      while ((used >> t) & 1ULL) {
+        const uint32_t en = a[t << 5];
+        if ((en >> 16) == (uint32_t)i) { vi = (int32_t)(en & 0xffffu); break; }
+        t = (t + 1u) & mask;
+      }
+    }
+    if (!found) {
+      if (room == 0u) return 0;
+      room--;
+      used |= 1ULL << s;
+    }
+    a[s << 5] = ((uint32_t)j << 16) | (uint32_t)vi;
+    return vj;
+  }
+};
+
+// slots per lane of the HashFY tables that fit a per-warp region of `bytes`
+__host__ __device__ inline uint32_t hashfy_slots(size_t bytes) {
+  uint32_t s = 64;
+  while (s > 1 && (size_t)s * 128 > bytes) s >>= 1;
+  return s;
+}
+
+// clear a whole map region (16-byte stores)
+__device__ __forceinline__ void fy_clear_region(uint32_t* fy, size_t bytes, int lane) {
+  uint4* p = reinterpret_cast<uint4*>(fy);
+  for (size_t k = lane; k < bytes / 16; k += 32) p[k] = make_uint4(0u, 0u, 0u, 0u);
 }
 
 __device__ __forceinline__ uint64_t win_bits(const uint64_t* w, uint32_t rel, uint32_t k) {
@@ -681,12 +758,15 @@ __device__ int warp_el_fy(SetCtx& c, const Tables& T, WarpScratch& ws, uint32_t*
                           int64_t e, uint64_t id, double winv) {
   const int64_t m = c.m;
   uint32_t ep = ws.epoch + 1;
-  if (ep >= (FY16 ? FY_EPOCHS16 : FY_EPOCHS32)) {  // epoch wrap: clear the map
+  if (ws.fy_dirty) {   // the lanes' hash maps were here (CTA kernels only): start over
+    fy_clear_region(fy, fy_region_bytes(m, FY16), lane);
+    ep = 1;
+  } else if (ep >= (FY16 ? FY_EPOCHS16 : FY_EPOCHS32)) {  // epoch wrap: clear the map
     fy_clear<FY16>(fy, m, lane);
     ep = 1;
   }
   __syncwarp();
-  if (lane == 0) ws.epoch = ep;
+  if (lane == 0) { ws.epoch = ep; ws.fy_dirty = 0u; }
   EpochFY<FY16> efy{fy, ep};
   uint64_t off = 0;
   int64_t i = 1;

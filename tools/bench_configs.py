@@ -81,7 +81,9 @@ def run_sketch(cfg, batch, algos, m):
         err = ctypes.c_int64(-1)
         _lib.check(L.pmh_status_check(status.data_ptr(), ctypes.byref(err), None), err.value)
         line = {"config": cfg, "algo": a, "m": m, "sets": S, "elements": N,
-                "ms_min": tmin, "ms_mean": tmean, "elements_per_s": N / (tmin / 1e3)}
+                "ms_min": tmin, "ms_mean": tmean, "elements_per_s": N / (tmin / 1e3),
+                # wrapping sum of all signature words: identical across builds
+                "sig_checksum": int(sig.sum().item())}
         print(json.dumps(line), flush=True)
         out[a] = sig.clone() if a == algos[-1] else None
     return sig

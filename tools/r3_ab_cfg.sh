@@ -5,7 +5,7 @@ for i in 1 2; do for L in $LIBS; do
 import json,sys
 out=[]
 for l in sys.stdin:
-    try: d=json.loads(l); out.append((d.get('algo'), round(d['ms_min'],2)))
+    try: d=json.loads(l); out.append((d.get('algo'), round(d['ms_min'],2), d.get('sig_checksum',0) % 100000))
     except Exception: pass
 print('$L'.split('/')[-1], out)
 "; done; done
