@@ -172,7 +172,7 @@ __device__ __forceinline__ bool run_batch(SetCtx& c, const Tables& T, const uint
     heavy = warp_ok && ctx_thr(c) > (double)c.heavy_pts * winv;
     if (!heavy) {
       if constexpr (HASHFY && family_uses_fy(F)) {
-        HashFY fy; fy.reset(fy_dense, lane, hashfy_slots(fy_region_bytes(c.m, FY16)));
+        HashFY<FY16> fy; fy.reset(fy_dense, lane, hashfy_slots(fy_region_bytes(c.m, FY16)));
         status = run_element<F>(c, T, fy, e, id, winv);
       } else {
         SparseFY fy; fy.reset();

@@ -107,42 +107,87 @@ __device__ __forceinline__ void fy_clear(uint32_t* fy, int64_t m, int lane) {
 // 64-bit register mask, so a new element starts with an O(1) reset.  The
 // register-resident SparseFY it replaces held 16 entries in 32 registers and
 // scanned all of them per step.
+// BLOOM (the large-m layout, 64 slots per lane filled to ~0.7): a hashed bit
+// per stored position ends most lookups without a probe (configs[2] uw4
+// 113 -> 106 ms, uw2 200 -> 189 ms); at m = 1024 (32 slots, <= 0.6) its two
+// registers cost the 80-register kernels more than the probes (PMH4 +4%).
+template <bool BLOOM>
 struct HashFY {
   uint32_t* a;        // region + lane
-  uint64_t used;
+  uint64_t used;      // slots in use
+  uint64_t bloom;     // one hashed bit per stored position: most lookups are of absent
+                      // positions (m >> steps) and end here, without a probe
   uint32_t mask;      // S - 1
   uint32_t room;      // entries left before the element goes to the warp path
   __device__ __forceinline__ void reset(uint32_t* region, int lane, uint32_t slots) {
     a = region + lane;
     used = 0ULL;
+    bloom = 0ULL;
     mask = slots - 1u;
     room = slots - (slots >> 3);   // load factor <= 7/8
+  }
+  static __device__ __forceinline__ uint32_t bloom_bit(uint32_t p) { return (p * 0x9E3779B1u) >> 26; }
+  // value stored for position p (p itself if absent); *slot = its slot, or -1
+  __device__ __forceinline__ int32_t lookup(uint32_t p, int* slot) const {
+    *slot = -1;
+    if (BLOOM && !((bloom >> bloom_bit(p)) & 1ULL)) return (int32_t)p;
+    uint32_t s = p & mask;
+    while ((used >> s) & 1ULL) {
+      const uint32_t en = a[s << 5];
+      if ((en >> 16) == p) { *slot = (int)s; return (int32_t)(en & 0xffffu); }
+      s = (s + 1u) & mask;
+    }
+    return (int32_t)p;
+  }
+  // first free slot at or (cyclically) after p's home slot: where linear
+  // probing inserts an absent position (bit scan of `used`, no memory access)
+  __device__ __forceinline__ uint32_t free_slot(uint32_t p) const {
+    const uint32_t s = p & mask;
+    const uint64_t all = mask == 63u ? ~0ULL : ((1ULL << (mask + 1u)) - 1ULL);
+    const uint64_t fr = ~used & all;
+    const uint64_t hi = fr & (~0ULL << s);
+    return (uint32_t)(__ffsll((long long)(hi ? hi : fr)) - 1);
   }
   // one lazy Fisher-Yates step (K:222-235): returns perm[j] and sets
   // perm[j] = perm[i] (both read before the write); 0 when the table is full
   __device__ __forceinline__ int32_t swap_step(int32_t i, int32_t j) {
-    int32_t vj = j, vi = i;
-    uint32_t s = (uint32_t)j & mask;
-    bool found = false;
-    while ((used >> s) & 1ULL) {
-      const uint32_t en = a[s << 5];
-      if ((en >> 16) == (uint32_t)j) { vj = (int32_t)(en & 0xffffu); found = true; break; }
-      s = (s + 1u) & mask;
-    }
-    if (i == j) {
-      vi = vj;
-    } else {
-      uint32_t t = (uint32_t)i & mask;
-      while ((used >> t) & 1ULL) {
-        const uint32_t en = a[t << 5];
-        if ((en >> 16) == (uint32_t)i) { vi = (int32_t)(en & 0xffffu); break; }
-        t = (t + 1u) & mask;
+    if constexpr (!BLOOM) {   // plain probes: the search for j ends on its insertion slot
+      int32_t vj = j, vi = i;
+      uint32_t s = (uint32_t)j & mask;
+      bool found = false;
+      while ((used >> s) & 1ULL) {
+        const uint32_t en = a[s << 5];
+        if ((en >> 16) == (uint32_t)j) { vj = (int32_t)(en & 0xffffu); found = true; break; }
+        s = (s + 1u) & mask;
       }
+      if (i == j) {
+        vi = vj;
+      } else {
+        uint32_t t = (uint32_t)i & mask;
+        while ((used >> t) & 1ULL) {
+          const uint32_t en = a[t << 5];
+          if ((en >> 16) == (uint32_t)i) { vi = (int32_t)(en & 0xffffu); break; }
+          t = (t + 1u) & mask;
+        }
+      }
+      if (!found) {
+        if (room == 0u) return 0;
+        room--;
+        used |= 1ULL << s;
+      }
+      a[s << 5] = ((uint32_t)j << 16) | (uint32_t)vi;
+      return vj;
     }
-    if (!found) {
+    int sj, si;
+    const int32_t vj = lookup((uint32_t)j, &sj);
+    const int32_t vi = i == j ? vj : lookup((uint32_t)i, &si);
+    uint32_t s = (uint32_t)sj;
+    if (sj < 0) {
       if (room == 0u) return 0;
       room--;
+      s = free_slot((uint32_t)j);
       used |= 1ULL << s;
+      if (BLOOM) bloom |= 1ULL << bloom_bit((uint32_t)j);
     }
     a[s << 5] = ((uint32_t)j << 16) | (uint32_t)vi;
     return vj;
