@@ -131,22 +131,22 @@ struct HashFY {
   __device__ __forceinline__ int32_t lookup(uint32_t p, int* slot) const {
     *slot = -1;
     if (BLOOM && !((bloom >> bloom_bit(p)) & 1ULL)) return (int32_t)p;
-    uint32_t s = p & mask;
+    uint32_t s = p & mask, k = 0u;
     while ((used >> s) & 1ULL) {
       const uint32_t en = a[s << 5];
       if ((en >> 16) == p) { *slot = (int)s; return (int32_t)(en & 0xffffu); }
-      s = (s + 1u) & mask;
+      s = (s + ++k) & mask;   // triangular probing (visits every slot of a 2^k table)
     }
     return (int32_t)p;
   }
-  // first free slot at or (cyclically) after p's home slot: where linear
-  // probing inserts an absent position (bit scan of `used`, no memory access)
+  // first free slot of p's probe sequence (a walk over the register mask, no
+  // memory access).  The lanes' tables fill to ~0.85 (a long unweighted-2
+  // element), where linear probing's clusters made an absent position's walk
+  // ~20 slots and every lane of the warp waits for the longest one.
   __device__ __forceinline__ uint32_t free_slot(uint32_t p) const {
-    const uint32_t s = p & mask;
-    const uint64_t all = mask == 63u ? ~0ULL : ((1ULL << (mask + 1u)) - 1ULL);
-    const uint64_t fr = ~used & all;
-    const uint64_t hi = fr & (~0ULL << s);
-    return (uint32_t)(__ffsll((long long)(hi ? hi : fr)) - 1);
+    uint32_t s = p & mask, k = 0u;
+    while ((used >> s) & 1ULL) s = (s + ++k) & mask;
+    return s;
   }
   // one lazy Fisher-Yates step (K:222-235): returns perm[j] and sets
   // perm[j] = perm[i] (both read before the write); 0 when the table is full

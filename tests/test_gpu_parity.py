@@ -176,3 +176,50 @@ def test_large_m_limits():
     from oracle import oracle as orc
     ref, _ = orc.sketch_csr("probminhash1", 6776, batch.ids, batch.weights, batch.offsets)
     assert (got != ref).sum() == 0
+
+
+@pytest.mark.parametrize("algo", ["unweighted1", "unweighted2", "unweighted3", "unweighted4"])
+@pytest.mark.parametrize("m,sizes", [
+    (4096, (255, 256, 300, 520, 700, 800, 850, 900, 950, 1000, 1100, 1500, 4000)),
+    (2048, (255, 256, 400, 450, 500, 600, 1000)),
+    (1024, (250, 256, 300, 380, 420, 470, 520, 700, 1000, 3000)),
+    (1000, (256, 300, 400, 500, 2000)),
+])
+def test_unweighted_lane_path_vs_oracle(algo, m, sizes):
+    """Unweighted sets of >= 256 elements run lane-per-element with the
+    Fisher-Yates families' per-lane hash maps (HashFY); the sizes straddle the
+    set-size cutoff (256) and the point counts where a lane's map fills up and
+    the element falls back to the warp path (~24 entries at m <= 1024, ~52 at
+    larger m)."""
+    from oracle import oracle as orc
+    from paper_1911_00675_b200 import datagen
+    rep = np.repeat(np.asarray(sizes, np.int64), 3)
+    st = datagen.CounterStream(1234 + m)
+    ids = st.words(int(rep.sum()))
+    off = np.concatenate([[0], np.cumsum(rep)]).astype(np.int64)
+    batch = datagen.CSRBatch(ids, None, off, "uw-lane")
+    ref, _ = orc.sketch_csr(algo, m, batch.ids, None, batch.offsets, threads=8)
+    got, _ = _gpu_sig(algo, m, batch)
+    assert (got != ref).sum() == 0
+
+
+@pytest.mark.parametrize("algo", ["probminhash2", "probminhash4"])
+@pytest.mark.parametrize("m", [512, 2048, 3000, 4096])
+def test_weighted_fy_hash_maps_vs_oracle(algo, m):
+    """Weighted Fisher-Yates families in the CTA kernel at signature sizes
+    whose map regions hold 32 / 64 hash slots per lane, with and without the
+    16-bit dense maps; equal weights inside a set make long lane sequences
+    (the map fills, the element moves to the warp path)."""
+    from oracle import oracle as orc
+    from paper_1911_00675_b200 import datagen
+    rng = np.random.default_rng(m)
+    sizes = np.concatenate([rng.integers(257, 3000, 12), [300, 600, 1200]]).astype(np.int64)
+    batch = datagen.random_sets(77 + m, sizes, "uniform")
+    w = batch.weights.copy()
+    off = batch.offsets
+    for s in range(0, len(sizes), 2):          # every other set: constant weights
+        w[off[s]:off[s + 1]] = 0.5 + 0.01 * s
+    batch = datagen.CSRBatch(batch.ids, w, off, "fy-hash")
+    ref, _ = orc.sketch_csr(algo, m, batch.ids, batch.weights, batch.offsets, threads=8)
+    got, _ = _gpu_sig(algo, m, batch)
+    assert (got != ref).sum() == 0
