@@ -118,7 +118,7 @@ __device__ __forceinline__ int32_t heavy_points_for(bool weighted, int64_t n, in
   if (n >= PMH_HEAVY_UW_MIN_N) h = weighted ? (double)PMH_HEAVY_POINTS_BIGN : (double)PMH_HEAVY_POINTS_UW;
   if constexpr (family_uses_fy(F)) {
     const uint32_t s = hashfy_slots(fy_region_bytes(m, FY16));
-    const double cap = (double)(s - (s >> 3)) - 4.0;   // HashFY::room less a margin
+    const double cap = (double)hashfy_room(s) - 4.0;   // HashFY::room less a margin
     if (h > cap) h = cap;
   }
   return (int32_t)h;

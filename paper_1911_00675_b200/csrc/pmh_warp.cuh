@@ -111,6 +111,14 @@ __device__ __forceinline__ void fy_clear(uint32_t* fy, int64_t m, int lane) {
 // per stored position ends most lookups without a probe (configs[2] uw4
 // 113 -> 106 ms, uw2 200 -> 189 ms); at m = 1024 (32 slots, <= 0.6) its two
 // registers cost the 80-register kernels more than the probes (PMH4 +4%).
+#ifndef PMH_HASHFY_ROOM_SHIFT
+#define PMH_HASHFY_ROOM_SHIFT 4
+#endif
+// entries a lane's table of `slots` takes (15/16 of it: 7/8 -> 15/16 sends fewer long
+// unweighted-2 elements to the warp path, configs[2] uw2 182 -> 177 ms)
+__host__ __device__ inline uint32_t hashfy_room(uint32_t slots) {
+  return slots - (slots >> PMH_HASHFY_ROOM_SHIFT);
+}
 template <bool BLOOM>
 struct HashFY {
   uint32_t* a;        // region + lane
@@ -124,7 +132,7 @@ struct HashFY {
     used = 0ULL;
     bloom = 0ULL;
     mask = slots - 1u;
-    room = slots - (slots >> 3);   // load factor <= 7/8
+    room = hashfy_room(slots);
   }
   static __device__ __forceinline__ uint32_t bloom_bit(uint32_t p) { return (p * 0x9E3779B1u) >> 26; }
   // value stored for position p (p itself if absent); *slot = its slot, or -1
