@@ -307,8 +307,13 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
   // Pull the range's ids into L2 while the weights are summed (the weights
   // arrive there by the sum itself): the element loop then reads its chunks
   // from L2 instead of HBM.
-  for (int64_t L = threadIdx.x; L * 16 < n; L += blockDim.x)
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(ids + L * 16));
+  // (not for weighted sets whose W is known, where the element loop is the
+  // first and only reader of the weights too: with ~440 sets in flight
+  // the prefetched lines of the large ones were evicted before their use --
+  // ncu showed the ids read twice from DRAM, at no gain in time)
+  if (!(family_weighted(F) && w && w_given > 0.0))
+    for (int64_t L = threadIdx.x; L * 16 < n; L += blockDim.x)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(ids + L * 16));
   double W;
   if (family_weighted(F) && w && w_given > 0.0) {
     // total weight known in advance (computed once per batch, or the caller's
