@@ -84,11 +84,19 @@ constexpr int SKETCH_THREADS = 256;
 // static __shared__ state too (SetShared and friends, < 1 KB)
 constexpr size_t SMEM_DYN_MAX = 227 * 1024 - 1024;
 
+// bytes of one warp's scratch in the CTA kernels (16-byte multiple)
+__host__ __device__ inline size_t scratch_bytes(int family) {
+  const size_t b = family_uses_fy(family)
+                       ? sizeof(WarpScratch)
+                       : offsetof(WarpScratch, words) + sizeof(uint64_t) * WIN_STATIC_WORDS;
+  return (b + 15) & ~(size_t)15;
+}
+
 __host__ __device__ inline size_t sketch_smem_bytes(int family, int64_t m, int threads,
                                                     bool fy16 = false) {
   const int nw = threads / 32;
   size_t b = sizeof(Slot) * (size_t)m;
-  b += sizeof(WarpScratch) * (size_t)nw;
+  b += scratch_bytes(family) * (size_t)nw;
   if (family_uses_fy(family)) b += fy_region_bytes(m, fy16) * (size_t)nw;
   return (b + 15) & ~(size_t)15;
 }
@@ -403,8 +411,8 @@ __device__ __forceinline__ void sketch_cta_setup(unsigned char* smem, int64_t m,
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   *slots = reinterpret_cast<Slot*>(smem);
-  *wscr = reinterpret_cast<WarpScratch*>(smem + sizeof(Slot) * m) + wid;
-  *fy_dense = reinterpret_cast<uint32_t*>(smem + sizeof(Slot) * m + sizeof(WarpScratch) * nwarps +
+  *wscr = reinterpret_cast<WarpScratch*>(smem + sizeof(Slot) * m + scratch_bytes(F) * (size_t)wid);
+  *fy_dense = reinterpret_cast<uint32_t*>(smem + sizeof(Slot) * m + scratch_bytes(F) * (size_t)nwarps +
                                           fy_region_bytes(m, FY16) * (size_t)wid);
   if (family_uses_fy(F)) {  // epoch 0 never matches: the map starts empty
     fy_clear<FY16>(*fy_dense, m, lane);

@@ -33,19 +33,25 @@ constexpr uint32_t WIN_BITS = 2048;  // 32 words
 #endif
 constexpr int SQ_CAP = 32 * (PMH_EPL + 1);
 
+// The fields the static families (labels with replacement) use come first:
+// their kernels allocate only that prefix per warp (scratch_bytes), which is
+// what lets three m = 4096 sets (64 KB slot tables) share an SM.
 struct WarpScratch {
-  uint64_t words[65];   // window (64 words for the parallel FY parse, +1 guard)
-  uint32_t eoff[32];    // window-relative bit offset of each point's first draw
-  int32_t lab[32];      // 1-based labels
   double dbuf[32];      // per-point increments of the ordered fold
   uint32_t q;           // points parsed
   uint32_t flags;       // bit0: batch ended by a slow path; bit1: fail
   uint64_t next_off;    // absolute bit offset after the batch
   uint32_t epoch;       // Fisher-Yates map epoch (one per warp-processed element)
   uint32_t fy_dirty;    // the map region last held the lanes' hash maps (HashFY): clear before use
-  uint32_t gm[32];      // parallel Fisher-Yates: lanes whose target is i0 + k
   int32_t sq[SQ_CAP];   // survivor queue of the large-set path (element indices, LIFO)
+  uint64_t words[65];   // window: 33-38 words for static offsets; 64 for the parallel
+                        // Fisher-Yates parse, +1 guard
+  // ---- Fisher-Yates families only ----
+  uint32_t eoff[32];    // window-relative bit offset of each point's first draw
+  int32_t lab[32];      // 1-based labels
+  uint32_t gm[32];      // parallel Fisher-Yates: lanes whose target is i0 + k
 };
+constexpr int WIN_STATIC_WORDS = 40;   // words[] entries the static families touch (<= 38)
 
 // Dense per-warp Fisher-Yates map with O(1) reset: entry = epoch << 16 | value
 // (the versioned lazy permutation of K:222-235 / lazyperm.py, one epoch per

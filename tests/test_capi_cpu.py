@@ -170,8 +170,8 @@ def test_nonstreaming_api_validation():
 
 
 @pytest.mark.parametrize("algo,m_bad", [("pminhash", 16385), ("minhash", 16385),
-                                        ("probminhash1", 13553), ("probminhash3a", 13553),
-                                        ("unweighted3", 13553), ("probminhash2", 6776),
+                                        ("probminhash1", 13841), ("probminhash3a", 13841),
+                                        ("unweighted3", 13841), ("probminhash2", 6776),
                                         ("probminhash4", 6776), ("unweighted4", 6776),
                                         ("superminhash", 65536)])
 def test_signature_size_limits_rejected_before_cuda(algo, m_bad):

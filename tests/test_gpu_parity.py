@@ -171,11 +171,13 @@ def test_large_m_limits():
     with pytest.raises(InvalidParamsError):
         _gpu_sig("probminhash2", 6776, batch)
     with pytest.raises(InvalidParamsError):
-        _gpu_sig("probminhash1", 13553, batch)
-    got, _ = _gpu_sig("probminhash1", 6776, batch)      # no Fisher-Yates map: fits
+        _gpu_sig("probminhash1", 13841, batch)
     from oracle import oracle as orc
-    ref, _ = orc.sketch_csr("probminhash1", 6776, batch.ids, batch.weights, batch.offsets)
-    assert (got != ref).sum() == 0
+    # no Fisher-Yates map: fits, up to the largest m of the static families
+    for algo, m in (("probminhash1", 6776), ("probminhash1", 13840), ("probminhash3", 13840)):
+        got, _ = _gpu_sig(algo, m, batch)
+        ref, _ = orc.sketch_csr(algo, m, batch.ids, batch.weights, batch.offsets)
+        assert (got != ref).sum() == 0, (algo, m)
 
 
 @pytest.mark.parametrize("algo", ["unweighted1", "unweighted2", "unweighted3", "unweighted4"])
