@@ -131,12 +131,16 @@ struct HashFY {
   uint64_t used;      // slots in use
   uint64_t bloom;     // one hashed bit per stored position: most lookups are of absent
                       // positions (m >> steps) and end here, without a probe
+  uint64_t low;       // BLOOM: exactly which positions < 64 are stored.  Step i looks up
+                      // position i (< 64 for the first 63 steps), stored only if an
+                      // earlier target fell that low: this lookup then never probes
   uint32_t mask;      // S - 1
   uint32_t room;      // entries left before the element goes to the warp path
   __device__ __forceinline__ void reset(uint32_t* region, int lane, uint32_t slots) {
     a = region + lane;
     used = 0ULL;
     bloom = 0ULL;
+    low = 0ULL;
     mask = slots - 1u;
     room = hashfy_room(slots);
   }
@@ -144,7 +148,10 @@ struct HashFY {
   // value stored for position p (p itself if absent); *slot = its slot, or -1
   __device__ __forceinline__ int32_t lookup(uint32_t p, int* slot) const {
     *slot = -1;
-    if (BLOOM && !((bloom >> bloom_bit(p)) & 1ULL)) return (int32_t)p;
+    if (BLOOM) {
+      if (p < 64u) { if (!((low >> p) & 1ULL)) return (int32_t)p; }
+      else if (!((bloom >> bloom_bit(p)) & 1ULL)) return (int32_t)p;
+    }
     uint32_t s = p & mask, k = 0u;
     while ((used >> s) & 1ULL) {
       const uint32_t en = a[s << 5];
@@ -201,7 +208,10 @@ struct HashFY {
       room--;
       s = free_slot((uint32_t)j);
       used |= 1ULL << s;
-      if (BLOOM) bloom |= 1ULL << bloom_bit((uint32_t)j);
+      if (BLOOM) {
+        if ((uint32_t)j < 64u) low |= 1ULL << j;
+        else bloom |= 1ULL << bloom_bit((uint32_t)j);
+      }
     }
     a[s << 5] = ((uint32_t)j << 16) | (uint32_t)vi;
     return vj;
