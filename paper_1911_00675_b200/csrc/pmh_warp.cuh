@@ -131,6 +131,7 @@ struct HashFY {
   uint64_t used;      // slots in use
   uint64_t bloom;     // one hashed bit per stored position: most lookups are of absent
                       // positions (m >> steps) and end here, without a probe
+  uint64_t bloom1;    // (second half of the 128-bit filter)
   uint64_t low;       // BLOOM: exactly which positions < 64 are stored.  Step i looks up
                       // position i (< 64 for the first 63 steps), stored only if an
                       // earlier target fell that low: this lookup then never probes
@@ -140,17 +141,21 @@ struct HashFY {
     a = region + lane;
     used = 0ULL;
     bloom = 0ULL;
+    bloom1 = 0ULL;
     low = 0ULL;
     mask = slots - 1u;
     room = hashfy_room(slots);
   }
-  static __device__ __forceinline__ uint32_t bloom_bit(uint32_t p) { return (p * 0x9E3779B1u) >> 26; }
+  static __device__ __forceinline__ uint32_t bloom_bit(uint32_t p) { return (p * 0x9E3779B1u) >> 25; }
   // value stored for position p (p itself if absent); *slot = its slot, or -1
   __device__ __forceinline__ int32_t lookup(uint32_t p, int* slot) const {
     *slot = -1;
     if (BLOOM) {
       if (p < 64u) { if (!((low >> p) & 1ULL)) return (int32_t)p; }
-      else if (!((bloom >> bloom_bit(p)) & 1ULL)) return (int32_t)p;
+      else {
+        const uint32_t bb = bloom_bit(p);
+        if (!((((bb & 64u) ? bloom1 : bloom) >> (bb & 63u)) & 1ULL)) return (int32_t)p;
+      }
     }
     uint32_t s = p & mask, k = 0u;
     while ((used >> s) & 1ULL) {
@@ -210,7 +215,10 @@ struct HashFY {
       used |= 1ULL << s;
       if (BLOOM) {
         if ((uint32_t)j < 64u) low |= 1ULL << j;
-        else bloom |= 1ULL << bloom_bit((uint32_t)j);
+        else {
+          const uint32_t bb = bloom_bit((uint32_t)j);
+          if (bb & 64u) bloom1 |= 1ULL << (bb & 63u); else bloom |= 1ULL << bb;
+        }
       }
     }
     a[s << 5] = ((uint32_t)j << 16) | (uint32_t)vi;
