@@ -117,6 +117,9 @@ __device__ __forceinline__ void fy_clear(uint32_t* fy, int64_t m, int lane) {
 // per stored position ends most lookups without a probe (configs[2] uw4
 // 113 -> 106 ms, uw2 200 -> 189 ms); at m = 1024 (32 slots, <= 0.6) its two
 // registers cost the 80-register kernels more than the probes (PMH4 +4%).
+#ifndef PMH_HASHFY_LINEAR
+#define PMH_HASHFY_LINEAR 1
+#endif
 #ifndef PMH_HASHFY_ROOM_SHIFT
 #define PMH_HASHFY_ROOM_SHIFT 4
 #endif
@@ -161,7 +164,11 @@ struct HashFY {
     while ((used >> s) & 1ULL) {
       const uint32_t en = a[s << 5];
       if ((en >> 16) == p) { *slot = (int)s; return (int32_t)(en & 0xffffu); }
+#if PMH_HASHFY_LINEAR
+      s = (s + 1u) & mask; (void)k;
+#else
       s = (s + ++k) & mask;   // triangular probing (visits every slot of a 2^k table)
+#endif
     }
     return (int32_t)p;
   }
@@ -170,9 +177,17 @@ struct HashFY {
   // element), where linear probing's clusters made an absent position's walk
   // ~20 slots and every lane of the warp waits for the longest one.
   __device__ __forceinline__ uint32_t free_slot(uint32_t p) const {
+#if PMH_HASHFY_LINEAR
+    const uint32_t s0 = p & mask;
+    const uint64_t all = mask == 63u ? ~0ULL : ((1ULL << (mask + 1u)) - 1ULL);
+    const uint64_t fr = ~used & all;
+    const uint64_t hi = fr & (~0ULL << s0);
+    return (uint32_t)(__ffsll((long long)(hi ? hi : fr)) - 1);
+#else
     uint32_t s = p & mask, k = 0u;
     while ((used >> s) & 1ULL) s = (s + ++k) & mask;
     return s;
+#endif
   }
   // one lazy Fisher-Yates step (K:222-235): returns perm[j] and sets
   // perm[j] = perm[i] (both read before the write); 0 when the table is full
