@@ -538,14 +538,18 @@ namespace pmh {
 // whole batch unchanged)
 constexpr int64_t SMALL_N = PMH_SMALL_N;
 constexpr int64_t SMALL_N_STATIC = PMH_SMALL_N_STATIC;
-#ifndef PMH_SMALL_N_SMALLM
-#define PMH_SMALL_N_SMALLM 512
-#endif
-// warp-per-set cutoff: for m <= 256 whole sets of up to 512 elements are cheap
-// enough for one warp (configs[3], configs[4]); for large m only tiny sets
+// warp-per-set cutoff: for large m only tiny sets; for m <= 256 whole sets are
+// cheap enough for one warp up to a few hundred elements (configs[3]: the
+// m <= 64 kernel of pmh_wps.cuh takes them all).  Above that the CTA kernel
+// wins, earlier for the Fisher-Yates families since their lanes got hash maps
+// (tools/uw_sweep.py, weighted sets at m = 128 / 256, n = 20 ... 500; configs[4],
+// m = 256, n = 500: ProbMinHash4 19.2 -> 17.5 ms)
 __host__ __device__ inline int64_t small_n_for(int family, int64_t m) {
   if (wps_eligible(family, m)) return (int64_t)WPS_NMAX;   // pmh_wps.cuh
-  if (m <= 256) return (int64_t)PMH_SMALL_N_SMALLM;
+  if (m <= 256) {
+    if (family_uses_fy(family)) return m <= 128 ? 384 : 128;
+    return m <= 128 ? 512 : 384;
+  }
   return family_uses_fy(family) ? SMALL_N : SMALL_N_STATIC;
 }
 
