@@ -182,6 +182,7 @@ struct HashFY {
     const uint64_t all = mask == 63u ? ~0ULL : ((1ULL << (mask + 1u)) - 1ULL);
     const uint64_t fr = ~used & all;
     const uint64_t hi = fr & (~0ULL << s0);
+    PMH_ASSERT(fr != 0ULL);   // room < slots: a free slot always exists
     return (uint32_t)(__ffsll((long long)(hi ? hi : fr)) - 1);
 #else
     uint32_t s = p & mask, k = 0u;
@@ -236,6 +237,7 @@ struct HashFY {
         }
       }
     }
+    PMH_ASSERT(s <= mask && j > 0 && j < 65536 && vi > 0 && vi < 65536);
     a[s << 5] = ((uint32_t)j << 16) | (uint32_t)vi;
     return vj;
   }
