@@ -113,18 +113,20 @@ __device__ __forceinline__ void fy_clear(uint32_t* fy, int64_t m, int lane) {
 // 64-bit register mask, so a new element starts with an O(1) reset.  The
 // register-resident SparseFY it replaces held 16 entries in 32 registers and
 // scanned all of them per step.
-// BLOOM (the large-m layout, 64 slots per lane filled to ~0.7): a hashed bit
-// per stored position ends most lookups without a probe (configs[2] uw4
-// 113 -> 106 ms, uw2 200 -> 189 ms); at m = 1024 (32 slots, <= 0.6) its two
-// registers cost the 80-register kernels more than the probes (PMH4 +4%).
-#ifndef PMH_HASHFY_LINEAR
-#define PMH_HASHFY_LINEAR 1
-#endif
+// BLOOM (the large-m layout: 64 slots per lane, filled to 0.7-0.9 by the 36-60
+// steps of a configs[2] element): register filters end most lookups -- nearly
+// all of them are of positions never stored, since m >> steps -- without a
+// probe: a 128-bit Bloom filter (one hashed bit per stored position) and an
+// exact mask of the stored positions < 64.  Insertion is a bit scan of `used`.
+// configs[2] uw4 113 -> 92 ms, uw2 200 -> 158 ms in all (a
+// triangular probe sequence was better only before the filters).  At
+// m = 1024 (32 slots, <= 0.6 full) the filters' registers cost the
+// 80-register kernels more than the probes (PMH4 +4%): plain probes there.
 #ifndef PMH_HASHFY_ROOM_SHIFT
 #define PMH_HASHFY_ROOM_SHIFT 4
 #endif
-// entries a lane's table of `slots` takes (15/16 of it: 7/8 -> 15/16 sends fewer long
-// unweighted-2 elements to the warp path, configs[2] uw2 182 -> 177 ms)
+// entries a lane's table of `slots` takes (15/16 of it: 7/8 sent three times as many
+// long unweighted-2 elements to the warp path, configs[2] uw2 +4%)
 __host__ __device__ inline uint32_t hashfy_room(uint32_t slots) {
   return slots - (slots >> PMH_HASHFY_ROOM_SHIFT);
 }
@@ -132,9 +134,7 @@ template <bool BLOOM>
 struct HashFY {
   uint32_t* a;        // region + lane
   uint64_t used;      // slots in use
-  uint64_t bloom;     // one hashed bit per stored position: most lookups are of absent
-                      // positions (m >> steps) and end here, without a probe
-  uint64_t bloom1;    // (second half of the 128-bit filter)
+  uint64_t bloom, bloom1;   // BLOOM: 128-bit filter, one hashed bit per stored position >= 64
   uint64_t low;       // BLOOM: exactly which positions < 64 are stored.  Step i looks up
                       // position i (< 64 for the first 63 steps), stored only if an
                       // earlier target fell that low: this lookup then never probes
@@ -160,35 +160,23 @@ struct HashFY {
         if (!((((bb & 64u) ? bloom1 : bloom) >> (bb & 63u)) & 1ULL)) return (int32_t)p;
       }
     }
-    uint32_t s = p & mask, k = 0u;
+    uint32_t s = p & mask;
     while ((used >> s) & 1ULL) {
       const uint32_t en = a[s << 5];
       if ((en >> 16) == p) { *slot = (int)s; return (int32_t)(en & 0xffffu); }
-#if PMH_HASHFY_LINEAR
-      s = (s + 1u) & mask; (void)k;
-#else
-      s = (s + ++k) & mask;   // triangular probing (visits every slot of a 2^k table)
-#endif
+      s = (s + 1u) & mask;
     }
     return (int32_t)p;
   }
-  // first free slot of p's probe sequence (a walk over the register mask, no
-  // memory access).  The lanes' tables fill to ~0.85 (a long unweighted-2
-  // element), where linear probing's clusters made an absent position's walk
-  // ~20 slots and every lane of the warp waits for the longest one.
+  // first free slot at or (cyclically) after p's home slot: where linear
+  // probing inserts an absent position (a bit scan of `used`, no memory access)
   __device__ __forceinline__ uint32_t free_slot(uint32_t p) const {
-#if PMH_HASHFY_LINEAR
     const uint32_t s0 = p & mask;
     const uint64_t all = mask == 63u ? ~0ULL : ((1ULL << (mask + 1u)) - 1ULL);
     const uint64_t fr = ~used & all;
     const uint64_t hi = fr & (~0ULL << s0);
     PMH_ASSERT(fr != 0ULL);   // room < slots: a free slot always exists
     return (uint32_t)(__ffsll((long long)(hi ? hi : fr)) - 1);
-#else
-    uint32_t s = p & mask, k = 0u;
-    while ((used >> s) & 1ULL) s = (s + ++k) & mask;
-    return s;
-#endif
   }
   // one lazy Fisher-Yates step (K:222-235): returns perm[j] and sets
   // perm[j] = perm[i] (both read before the write); 0 when the table is full

@@ -20,7 +20,7 @@ sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 for m in ms_:
     for n in ns:
         S = max(296, total // n)
-        weighted = any(a.startswith("prob") for a in algos)   # Exp(1) weights for the weighted variants
+        weighted = any(a.startswith(("prob", "pmin")) for a in algos)   # Exp(1) weights for the weighted variants
         b = datagen.random_sets(11, [n] * S, "exp") if weighted else datagen.config3(S, n, seed=11)
         ids, off = to_device_u64(b.ids), to_device_i64(b.offsets)
         wd = to_device_f64(b.weights) if weighted else None
