@@ -143,6 +143,7 @@ __device__ __forceinline__ int32_t heavy_points_for(bool weighted, int64_t n, in
 // to be long (or whose Fisher-Yates state outgrows the lane map) run
 // warp-cooperatively.
 struct SharedGrab {
+  static constexpr bool shared = true;
   unsigned* ctr;
   unsigned chunk;
   __device__ __forceinline__ unsigned next(int lane) {
@@ -152,6 +153,7 @@ struct SharedGrab {
   }
 };
 struct LocalGrab {
+  static constexpr bool shared = false;
   unsigned cur;
   unsigned chunk;
   __device__ __forceinline__ unsigned next(int) { const unsigned b = cur; cur += chunk; return b; }
@@ -246,6 +248,20 @@ __device__ __forceinline__ void warp_elements(SetCtx& c, const Tables& T, const 
   for (;;) {
     const uint32_t base = grab.next(lane);
     const bool more = base < n32;
+#ifndef PMH_ROLL_PREFETCH
+#define PMH_ROLL_PREFETCH 8   // chunks ahead (0: off)
+#endif
+    if constexpr (Grab::shared && PMH_ROLL_PREFETCH > 0) {
+      // rolling L2 prefetch: the chunk some warp of the CTA will grab
+      // PMH_ROLL_PREFETCH grabs from now (lanes 0-7: its ids lines, 16-23: its
+      // weights), so the element loads below find L2 instead of HBM latency
+      const uint32_t o = 16u * (uint32_t)(lane & 15);
+      const uint32_t pe = base + ch * PMH_ROLL_PREFETCH + o;
+      if (o < ch && pe < n32) {
+        if (lane < 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(ids + pe));
+        else if (family_weighted(F) && w) asm volatile("prefetch.global.L2 [%0];" ::"l"(w + pe));
+      }
+    }
     if (more) {
       uint64_t id[PMH_EPL];
       double wv[PMH_EPL];
