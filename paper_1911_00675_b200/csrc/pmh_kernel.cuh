@@ -420,6 +420,15 @@ __device__ __forceinline__ bool sketch_range(const SketchArgs& a, int64_t off, i
 #ifndef SKETCH_MINBLOCKS
 #define SKETCH_MINBLOCKS 3   // 80 registers, 3 CTAs/SM: measured 3-12% faster than 2
 #endif
+// ProbMinHash1 (labels with replacement, log1p points: the smallest per-lane
+// state) gains from a fourth CTA per SM even at 64 registers with ~220 bytes
+// of spills (configs[1]: 3.49 -> 3.18 ms); ProbMinHash2 / 4 lose 5-10% there
+// (and their shared memory holds three CTAs anyway), ProbMinHash3 is unchanged.
+#ifndef PMH_MINBLOCKS_PMH1
+#define PMH_MINBLOCKS_PMH1 4
+#endif
+template <int F>
+constexpr int sketch_minblocks() { return F == FAM_PMH1 ? PMH_MINBLOCKS_PMH1 : SKETCH_MINBLOCKS; }
 
 template <int F, bool FY16>
 __device__ __forceinline__ void sketch_cta_setup(unsigned char* smem, int64_t m, Slot** slots,
@@ -440,7 +449,7 @@ __device__ __forceinline__ void sketch_cta_setup(unsigned char* smem, int64_t m,
 // so the other instantiations carry no trace of it (these kernels are
 // instruction-cache bound)
 template <int F, int NT = SKETCH_THREADS, bool FY16 = false>
-__global__ void __launch_bounds__(NT, (NT == SKETCH_THREADS ? SKETCH_MINBLOCKS : 1))
+__global__ void __launch_bounds__(NT, (NT == SKETCH_THREADS ? sketch_minblocks<F>() : 1))
     sketch_sets_kernel(SketchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SetShared sh;
@@ -491,7 +500,7 @@ __global__ void __launch_bounds__(NT, (NT == SKETCH_THREADS ? SKETCH_MINBLOCKS :
 // Parts of the split sets (pmh_split.cuh): persistent CTAs, each part's
 // verified minima merged into the set's global table.
 template <int F, bool FY16 = false>
-__global__ void __launch_bounds__(SKETCH_THREADS, SKETCH_MINBLOCKS)
+__global__ void __launch_bounds__(SKETCH_THREADS, sketch_minblocks<F>())
     sketch_split_kernel(SketchArgs a, SplitArgs sp) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SetShared sh;
