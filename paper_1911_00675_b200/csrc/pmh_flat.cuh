@@ -95,7 +95,10 @@ __device__ __noinline__ bool flat_slow_point(SetCtx& c, const Tables& T, uint64_
 // prefilter, which the per-round scans here cannot match when almost every
 // element has a single candidate point.
 template <int F>
-__global__ void __launch_bounds__(FLAT_THREADS, 3) sketch_flat_kernel(SketchArgs a) {
+#ifndef PMH_FLAT_MINB
+#define PMH_FLAT_MINB 4   // 64 registers: configs[1] ProbMinHash3 2.50 -> 2.45 ms (2: 2.75; 5-6: see DESIGN)
+#endif
+__global__ void __launch_bounds__(FLAT_THREADS, PMH_FLAT_MINB) sketch_flat_kernel(SketchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ FlatShared sh;
   Slot* slots = reinterpret_cast<Slot*>(smem);
