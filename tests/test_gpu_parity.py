@@ -225,3 +225,22 @@ def test_weighted_fy_hash_maps_vs_oracle(algo, m):
     ref, _ = orc.sketch_csr(algo, m, batch.ids, batch.weights, batch.offsets, threads=8)
     got, _ = _gpu_sig(algo, m, batch)
     assert (got != ref).sum() == 0
+
+
+@pytest.mark.parametrize("algo", ["probminhash1", "probminhash2", "probminhash3", "probminhash4",
+                                  "unweighted3", "unweighted4"])
+@pytest.mark.parametrize("m", [100, 128, 256])
+def test_small_m_kernel_cutoffs_vs_oracle(algo, m):
+    """m <= 256: sets around the warp-per-set / CTA-kernel cutoffs (128, 384 and
+    512 elements, per family, pmh_kernel.cuh: small_n_for) and around the flat
+    kernel's (255 for the unweighted family, 1024 otherwise)."""
+    from oracle import oracle as orc
+    from paper_1911_00675_b200 import datagen
+    sizes = np.array([1, 7, 100, 127, 128, 129, 254, 255, 256, 257, 383, 384, 385, 511, 512, 513,
+                      600, 1023, 1024, 1025, 1500], np.int64)
+    batch = datagen.random_sets(4242 + m, sizes, "exp")
+    if algo.startswith("unweighted"):
+        batch = type(batch)(batch.ids, None, batch.offsets, batch.name)
+    ref, _ = orc.sketch_csr(algo, m, batch.ids, batch.weights, batch.offsets, threads=8)
+    got, _ = _gpu_sig(algo, m, batch)
+    assert (got != ref).sum() == 0
