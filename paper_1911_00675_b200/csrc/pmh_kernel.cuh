@@ -553,14 +553,18 @@ namespace pmh {
 #ifndef PMH_SMALL_N_STATIC
 #define PMH_SMALL_N_STATIC 7
 #endif
-// sets up to this size run warp-per-set at large m (measured on configs[1]:
-// cutoff 7 vs 3 is 2% / 6% faster for ProbMinHash 1 / 3 and 4% slower for
-// the Fisher-Yates families 2 / 4, whose warp-per-set map costs more).  The
+// sets up to this size run warp-per-set at large m (measured on configs[1]
+// in round 1: cutoff 7 vs 3 is 2% / 6% faster for ProbMinHash 1 / 3 and 4%
+// slower for the Fisher-Yates families 2 / 4, whose warp-per-set map costs
+// more; ProbMinHash1 has its own cutoff since, small_n_for below).  The
 // Fisher-Yates families send only singletons there: a warp runs a set's long
 // elements one after another, and 2-3 elements of ~m points each made those
 // sets the latency floor of a small batch (1/8 shard of configs[1]: the
 // n < 4 class 0.89 -> 0.38 ms for ProbMinHash2, 0.53 -> 0.25 for 4; the
 // whole batch unchanged)
+#ifndef PMH_SMALL_N_PMH1
+#define PMH_SMALL_N_PMH1 3
+#endif
 constexpr int64_t SMALL_N = PMH_SMALL_N;
 constexpr int64_t SMALL_N_STATIC = PMH_SMALL_N_STATIC;
 // warp-per-set cutoff: for large m only tiny sets; for m <= 256 whole sets are
@@ -575,7 +579,10 @@ __host__ __device__ inline int64_t small_n_for(int family, int64_t m) {
     if (family_uses_fy(family)) return m <= 128 ? 384 : 128;
     return m <= 128 ? 512 : 384;
   }
-  return family_uses_fy(family) ? SMALL_N : SMALL_N_STATIC;
+  if (family_uses_fy(family)) return SMALL_N;
+  // ProbMinHash1 since its CTA kernel runs four CTAs per SM: 3 (configs[1]:
+  // 3.19 -> 3.09 ms; 1: 3.30, 2: 3.10, 5: 3.15, 7: 3.19, 15: 3.23)
+  return family == FAM_PMH1 ? (int64_t)PMH_SMALL_N_PMH1 : SMALL_N_STATIC;
 }
 
 struct WarpSetVars {
