@@ -5,9 +5,11 @@
 // element; elements whose expected point count w * thr is small are run
 // lane-per-element through the reference recurrence (pmh_sketch.cuh, "mode
 // A"); long elements (small sets, heavy weights) and Fisher-Yates elements
-// that outgrow the per-lane sparse map are run warp-cooperatively
-// (pmh_warp.cuh, "mode B").  The final verification max_k h_k <= t makes the
-// threshold guess t exact-safe (retry with a larger t otherwise).
+// that outgrow the lane's hash map are run warp-cooperatively (pmh_warp.cuh,
+// "mode B"); unweighted sets of >= 256 elements keep their equal-length
+// elements on the lanes (heavy_points_for).  The final verification
+// max_k h_k <= t makes the threshold guess t exact-safe (retry with a larger
+// t otherwise).
 #pragma once
 #include "pmh_warp.cuh"
 #include "pmh_split.cuh"

@@ -14,8 +14,10 @@
 //      recurrence (Appendix A), skipping every point whose value -- or a
 //      provable lower bound of it, which avoids log1p -- exceeds
 //      thr = min(t, h_max);
-//   3. hands elements whose lazy Fisher-Yates state outgrows the per-thread
-//      sparse map to warp-cooperative processing with a dense shared map;
+//   3. hands elements whose lazy Fisher-Yates state outgrows the lane's map
+//      (a per-lane hash table in shared memory, pmh_warp.cuh: HashFY; a small
+//      register map in the warp-per-set kernel) to warp-cooperative processing
+//      with a dense shared map;
 //   4. verifies max_k h_k <= t (else retries with a larger t; re-offering a
 //      point is idempotent) and writes sig_k = ids[argmin].
 #pragma once
