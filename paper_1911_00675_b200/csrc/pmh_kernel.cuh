@@ -220,7 +220,23 @@ __device__ __forceinline__ bool run_batch(SetCtx& c, const Tables& T, const uint
 #define PMH_REFRESH_ON_CHANGE 0
 #endif
   const bool changed = PMH_REFRESH_ON_CHANGE && __any_sync(0xffffffffu, c.updates != upd0);
-  const bool trig = __any_sync(0xffffffffu, c.trig);
+  // ... and, for unweighted sets, the FIRST refresh: their table fills only at
+  // ~93% of the work (every element contributes equally), in the middle of
+  // long lane batches, and the lane whose offer filled the last slot may be
+  // deep inside another warp's batch.  The first warp that ends a batch with
+  // the table full and no stop limit yet computes it; the other warps' lanes
+  // read h_max at every step (configs[2] uw2 158 -> 150 ms, uw1 / uw4 -0.5 /
+  // -0.8%, uw3 +0.6%; on weighted sets the check cost the configs[1] step 0.2%)
+#ifndef PMH_FIRST_REFRESH
+#define PMH_FIRST_REFRESH 1
+#endif
+  bool first = false;
+  if (PMH_FIRST_REFRESH && !w && lane == 0 &&
+      *(volatile unsigned long long*)c.hmax_bits == EMPTY_H &&
+      *(volatile unsigned*)c.filled >= (unsigned)c.m)
+    // one warp only: EMPTY_H - 1 is still an upper bound of every slot
+    first = atomicCAS(c.hmax_bits, EMPTY_H, EMPTY_H - 1ULL) == EMPTY_H;
+  const bool trig = __any_sync(0xffffffffu, c.trig || first);
   c.trig = false;
   if (changed || trig || ++c.since_refresh >= PMH_REFRESH_EVERY) {
     hmax_refresh_warp(c, lane);
